@@ -1,0 +1,189 @@
+/* crius.h -- C-ABI of libcrius, the B200-native Crius Cell estimator.
+ *
+ * Crius (arXiv 2403.16125, /root/reference/PAPER.md, cited P:<line>) shards a
+ * cluster's scheduling space into Cells: a job with a fixed GPU type, GPU
+ * count and pipeline-stage count ("Cell"), estimates every Cell
+ * ("Agile Cell Estimation") and schedules jobs on Cells (Alg. 1,
+ * P:432-464).  This library computes that hot path on one GPU:
+ *
+ *   crius_load_profiles    profiles -> device (decoupled compute/comm)
+ *   crius_enumerate_cells  Cells of every job
+ *   crius_estimate_cells   stage split (P:266-283 read as a min-max DP, §N3),
+ *                          every DP x TP x microbatch plan (§N5),
+ *                          best plan per Cell
+ *   crius_schedule_round   one scheduling round (Alg. 1)
+ *
+ * The normative formulas are SURVEY.md §N0-§N6 (part of the contract), the
+ * readings of the paper are listed in DESIGN.md.  Everything here is plain C:
+ * fixed-width integers, host or device pointers, sizes.  Streams are passed as
+ * `void *` holding a cudaStream_t (NULL = legacy default stream).
+ *
+ * Arithmetic.  Every decision-path quantity is an integer: int64 ns, int64
+ * bytes, alpha in ns, beta in ns per MiB (2^20 B).  Every degree (G, S, g, tp,
+ * dp, B, GB, cap, gpn, g_max) is a power of two.  fp64 appears only in the
+ * round's scores (IEEE, no FMA contraction).  Results are bit-reproducible
+ * and independent of the number of GPUs the Cell space is sharded over.
+ *
+ * Errors.  Every call returns a crius_status; crius_last_error() gives a
+ * thread-local message for the last failing call.  A Cell with no feasible
+ * plan is data (plan = -1, t_ns = INT64_MAX), not an error.  Asynchronous
+ * CUDA faults surface as CRIUS_ECUDA at the next synchronising call.
+ *
+ * Threads.  One context per device; calls on one context are not thread-safe.
+ */
+#ifndef CRIUS_H
+#define CRIUS_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct crius_ctx crius_ctx; /* opaque, owned by the library */
+
+typedef enum {
+  CRIUS_OK = 0,
+  CRIUS_EINVAL = 2,      /* bad argument, non-power-of-two degree, bound violated */
+  CRIUS_EINFEASIBLE = 3, /* the enumeration produced zero Cells */
+  CRIUS_ECUDA = 4,       /* CUDA runtime error (message has the CUDA string) */
+  CRIUS_ENOMEM = 5,      /* device allocation failed */
+  CRIUS_ESTATE = 6       /* call out of order (e.g. estimate before enumerate) */
+} crius_status;
+
+/* GPU types (Table sim_cluster).  Host pointers, read during the
+ * call only.  capacity and gpus_per_node are powers of two (A-19, A-20). */
+typedef struct {
+  int32_t n_types;                 /* 1..16 */
+  const int32_t *capacity;         /* [n_types] GPUs of this type in the cluster */
+  const int32_t *gpus_per_node;    /* [n_types] node size: link class boundary (A-15) */
+  const int64_t *mem_bytes;        /* [n_types] per-GPU memory (memory filter) */
+  const int64_t *alpha_intra_ns;   /* [n_types] alpha-beta of the intra-node link (D3) */
+  const int64_t *beta_intra_ns_per_mib;
+  const int64_t *alpha_inter_ns;   /* [n_types] inter-node link */
+  const int64_t *beta_inter_ns_per_mib;
+} crius_cluster;
+
+/* Jobs and their profiles (decoupled computation/communication).
+ * Host pointers, read during the call only. */
+typedef struct {
+  int32_t n_jobs;                  /* >= 1 */
+  int32_t k_max;                   /* compute profiled for tp = 2^0 .. 2^k_max, k_max <= 6 */
+  const int64_t *job_id;           /* [n_jobs] unique; priority = (submit, id) ascending (A-18) */
+  const int64_t *submit_time;      /* [n_jobs] */
+  const int32_t *n_gpus_req;       /* [n_jobs] N_G given by the user, power of two */
+  const int32_t *global_batch;     /* [n_jobs] GB, power of two */
+  const int32_t *k_state;          /* [n_jobs] bytes of state per param byte (A-13), >= 1 */
+  const int32_t *n_layers;         /* [n_jobs] L >= 1 (operator chain) */
+  const int64_t *layer_off;        /* [n_jobs+1] exclusive prefix of n_layers */
+  const int32_t *compute_ns;       /* [n_types][k_max+1][total_layers] ns per sample, fwd+bwd,
+                                      at tp = 2^k; every entry >= 1 */
+  const int64_t *param_bytes;      /* [total_layers] w */
+  const int64_t *act_bytes;        /* [total_layers] stored activation bytes per sample */
+  const int64_t *boundary_bytes;   /* [total_layers] bytes per sample sent to the next stage */
+  const int64_t *tp_bytes;         /* [total_layers] TP all-reduce bytes per sample */
+  const int32_t *tp_calls;         /* [total_layers] TP all-reduce calls per microbatch */
+} crius_jobs;
+
+typedef struct {
+  int32_t gpu_set;     /* 0 = paper {N_G/2, N_G, 2N_G}; 1 = all powers of two <= capacity */
+  int32_t s_max;       /* stage-count cap (S in {1,2,4,..} <= min(G, L, s_max), A-6) */
+  int32_t g_max;       /* per-stage GPU cap: G/S <= g_max <= 2^k_max */
+  int32_t b_mode;      /* 0 = B = 4*S microbatches (GPipe); 1 = the list below */
+  int32_t b_count;     /* b_mode 1: 1..16 ascending powers of two */
+  const int32_t *b_values;
+  int32_t search_depth; /* d in [0, 16]: victim moves per trial and reverse-scaling sweeps
+                           (default 3 at P:737; A-17) */
+} crius_config;
+
+/* One per Cell, 16 bytes.  t_ns = best T_iter (int64 ns) or INT64_MAX;
+ * plan = p = k*nB + b (tp = 2^k, B = Bset[b]) or -1; flags bit 0 = feasible.
+ * The estimate in seconds is (double)t_ns / 1e9. */
+typedef struct {
+  int64_t t_ns;
+  int32_t plan;
+  int32_t flags;
+} crius_cell_result;
+
+/* Read-only DEVICE view of the Cell table (SoA, §N2 order: job, type, G asc,
+ * S asc).  Cell ids are positions in this order.  Valid until crius_destroy. */
+typedef struct {
+  int64_t n_cells, n_cell_plans, n_units; /* unit = (job, type) = j*n_types + t */
+  const int32_t *job, *type, *G, *S, *nplans;   /* [n_cells] */
+  const int64_t *plan_off;                      /* [n_cells] global plan offset */
+  const int64_t *unit_cell_begin;               /* [n_units+1] */
+  const int64_t *unit_plan_begin;               /* [n_units+1] */
+} crius_cell_view;
+
+/* Validate inputs (SURVEY §N0 bounds: L*max(c)*GB < 2^52, every T_iter < 2^62,
+ * kst*sum(w) + GB*sum(act) < 2^62, ...), copy them H2D into library-owned
+ * SoA buffers on `device` (enqueued on `stream`, synchronised before return),
+ * and compute the round's priority order.  On success *out owns the context.
+ * EINVAL names the first violated rule. */
+crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cluster,
+                                 const crius_jobs *jobs, const crius_config *config,
+                                 int32_t device, void *stream);
+
+/* Re-copy new profile VALUES of the same shape (same n_types, n_jobs,
+ * n_layers, k_max, config) into the existing buffers; validates like load.
+ * Invalidates previous enumeration/estimates (call enumerate again). */
+crius_status crius_update_profiles(crius_ctx *ctx, const crius_cluster *cluster,
+                                   const crius_jobs *jobs, void *stream);
+
+/* Enumerate every Cell (§N2) on the device: per-unit counts, scan,
+ * fill.  Synchronises `stream` and returns the counts.  EINFEASIBLE if 0 Cells. */
+crius_status crius_enumerate_cells(crius_ctx *ctx, int64_t *n_cells, int64_t *n_cell_plans,
+                                   int64_t *n_units, void *stream);
+
+/* Device view of the Cell table (after enumerate). */
+crius_status crius_cells(crius_ctx *ctx, crius_cell_view *view);
+
+/* int16 entries per unit in the optional d_splits output of estimate; the
+ * split of S = 2^si for unit u is at (u - unit_begin)*stride + (2^si - 1) + si,
+ * S+1 boundaries b_0=0 < b_1 < .. < b_S = L (stage s covers layers [b_s, b_{s+1}));
+ * entries of S values the unit does not use are -1. */
+int32_t crius_split_stride(const crius_ctx *ctx);
+
+/* Contiguous unit ranges for `world` ranks, balanced by per-unit work weight
+ * (SURVEY §8(e)); host outputs unit_begin[world+1], cell_begin[world+1].
+ * Synchronous (small D2H). */
+crius_status crius_partition_units(crius_ctx *ctx, int32_t world, int64_t *unit_begin,
+                                   int64_t *cell_begin, void *stream);
+
+/* Estimate every Cell of units [unit_begin, unit_end): one fused kernel does
+ * the per-unit prefix staging, the min-max stage DP with the lowest-argmin tie
+ * rule R0 (A-4), the cost of every plan (§N5) and the per-Cell argmin (lowest
+ * plan index wins ties, A-10).  d_out (caller-owned DEVICE buffer) receives one
+ * record per Cell: d_out[i] = Cell (unit_cell_begin[unit_begin] + i).
+ * d_splits (optional DEVICE int16 buffer or NULL) receives the splits.
+ * Asynchronous on `stream`. */
+crius_status crius_estimate_cells(crius_ctx *ctx, int64_t unit_begin, int64_t unit_end,
+                                  crius_cell_result *d_out, int16_t *d_splits, void *stream);
+
+/* Undo per-rank padding after an all-gather: d_gathered holds `world` chunks of
+ * `chunk_stride` records, chunk r = Cells [cell_begin[r], cell_begin[r+1]) (host
+ * array from crius_partition_units); writes d_all[n_cells].  Asynchronous. */
+crius_status crius_compact_gathered(crius_ctx *ctx, const crius_cell_result *d_gathered,
+                                    int64_t chunk_stride, int32_t world,
+                                    const int64_t *cell_begin, crius_cell_result *d_all,
+                                    void *stream);
+
+/* One scheduling round (§N6: Phase A SchedArrival P:436-445 with ScaleResource
+ * P:491-497 at search depth d, Phase B extra scheduling / reverse scaling
+ * P:449-450) over all Cells, on the device.  d_all: DEVICE results of
+ * every Cell.  free_gpus: HOST [n_types] or NULL (= capacity).  Outputs (HOST):
+ * decision[n_jobs] = Cell id | -1 pending | -2 unschedulable; free_after[n_types];
+ * *total_score = sum of normalised throughputs (A-16) in priority order.
+ * Synchronises `stream`. */
+crius_status crius_schedule_round(crius_ctx *ctx, const crius_cell_result *d_all,
+                                  const int32_t *free_gpus, int64_t *decision,
+                                  int32_t *free_after, double *total_score, void *stream);
+
+/* Number of kernels this context has launched so far (for launch accounting). */
+int64_t crius_kernel_launches(const crius_ctx *ctx);
+
+const char *crius_last_error(void);
+void crius_destroy(crius_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CRIUS_H */

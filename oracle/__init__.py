@@ -1,0 +1,150 @@
+"""ctypes front-end of the CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this package.  The product path (paper_2403_16125_b200) never
+does, and shares no code with it; both only consume the seeded arrays of
+paper_2403_16125_b200.workload.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "libcrius_oracle.so")
+SRC = os.path.join(HERE, "crius_oracle.cpp")
+INF = np.iinfo(np.int64).max
+
+
+def build(force=False):
+    """g++ -O2, single thread, no FMA contraction, no fast-math."""
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(
+            os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "crius_oracle.h"))):
+        return LIB
+    subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math",
+                           "-shared", "-fPIC", "-o", LIB, SRC])
+    return LIB
+
+
+class _Problem(C.Structure):
+    _fields_ = [
+        ("n_types", C.c_int32), ("cap", C.c_void_p), ("gpn", C.c_void_p), ("mem", C.c_void_p),
+        ("alpha_in", C.c_void_p), ("beta_in", C.c_void_p), ("alpha_x", C.c_void_p),
+        ("beta_x", C.c_void_p), ("n_jobs", C.c_int32), ("k_max", C.c_int32),
+        ("job_id", C.c_void_p), ("submit", C.c_void_p), ("ng", C.c_void_p), ("gb", C.c_void_p),
+        ("kst", C.c_void_p), ("n_layers", C.c_void_p), ("layer_off", C.c_void_p),
+        ("c", C.c_void_p), ("w", C.c_void_p), ("act", C.c_void_p), ("bnd", C.c_void_p),
+        ("tpv", C.c_void_p), ("tpn", C.c_void_p), ("gpu_set", C.c_int32), ("s_max", C.c_int32),
+        ("g_max", C.c_int32), ("b_mode", C.c_int32), ("b_count", C.c_int32),
+        ("b_values", C.c_void_p), ("depth", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        _lib.oracle_comm.restype = C.c_int64
+        _lib.oracle_comm.argtypes = [C.c_int32] + [C.c_int64] * 5
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Oracle:
+    """Holds a Problem's arrays (kept alive) and the ctypes struct."""
+
+    def __init__(self, pr):
+        self.pr = pr
+        keep = {}
+
+        def arr(name, dtype):
+            a = np.ascontiguousarray(getattr(pr, name), dtype=dtype)
+            keep[name] = a
+            return _ptr(a)
+
+        bv = np.ascontiguousarray(pr.b_values, np.int32)
+        if bv.size == 0:
+            bv = np.zeros(1, np.int32)
+        keep["b_values"] = bv
+        self._keep = keep
+        self.s = _Problem(
+            n_types=pr.n_types, cap=arr("cap", np.int32), gpn=arr("gpn", np.int32),
+            mem=arr("mem", np.int64), alpha_in=arr("alpha_in", np.int64),
+            beta_in=arr("beta_in", np.int64), alpha_x=arr("alpha_x", np.int64),
+            beta_x=arr("beta_x", np.int64), n_jobs=pr.n_jobs, k_max=pr.k_max,
+            job_id=arr("job_id", np.int64), submit=arr("submit", np.int64), ng=arr("ng", np.int32),
+            gb=arr("gb", np.int32), kst=arr("kst", np.int32), n_layers=arr("n_layers", np.int32),
+            layer_off=arr("layer_off", np.int64), c=arr("c", np.int32), w=arr("w", np.int64),
+            act=arr("act", np.int64), bnd=arr("bnd", np.int64), tpv=arr("tpv", np.int64),
+            tpn=arr("tpn", np.int32), gpu_set=pr.gpu_set, s_max=pr.s_max, g_max=pr.g_max,
+            b_mode=pr.b_mode, b_count=int(pr.b_values.size) if pr.b_mode == 1 else 0,
+            b_values=_ptr(bv), depth=pr.depth)
+        self.L = lib()
+
+    def _check(self, rc, what):
+        if rc != 0:
+            raise RuntimeError(f"oracle {what} failed with code {rc}")
+
+    def count(self):
+        n, p = C.c_int64(), C.c_int64()
+        self._check(self.L.oracle_count(C.byref(self.s), C.byref(n), C.byref(p)), "count")
+        return n.value, p.value
+
+    def enumerate(self):
+        n, _ = self.count()
+        out = {k: np.zeros(n, np.int32) for k in ("job", "type", "G", "S", "nplans")}
+        self._check(self.L.oracle_enumerate(C.byref(self.s), *[_ptr(out[k]) for k in
+                                                                ("job", "type", "G", "S", "nplans")]),
+                    "enumerate")
+        return out
+
+    def split(self, j, t, S):
+        b = np.zeros(S + 1, np.int32)
+        self._check(self.L.oracle_split(C.byref(self.s), j, t, S, _ptr(b)), "split")
+        return b
+
+    def plan_cost(self, j, t, G, S, p):
+        T = np.zeros(S, np.int64)
+        sy = np.zeros(S, np.int64)
+        mem = np.zeros(S, np.int64)
+        ti = C.c_int64()
+        fe = C.c_int32()
+        self._check(self.L.oracle_plan_cost(C.byref(self.s), j, t, G, S, p, _ptr(T), _ptr(sy),
+                                            _ptr(mem), C.byref(ti), C.byref(fe)), "plan_cost")
+        return dict(T=T, sync=sy, mem=mem, t_iter=ti.value, feasible=bool(fe.value))
+
+    def estimate(self, cells, c0=0, c1=None):
+        n = len(cells["job"])
+        c1 = n if c1 is None else c1
+        t_ns = np.zeros(c1 - c0, np.int64)
+        plan = np.zeros(c1 - c0, np.int32)
+        self._check(self.L.oracle_estimate(C.byref(self.s), *[_ptr(cells[k]) for k in
+                                                              ("job", "type", "G", "S", "nplans")],
+                                           C.c_int64(c0), C.c_int64(c1), _ptr(t_ns), _ptr(plan)),
+                    "estimate")
+        return t_ns, plan
+
+    def round(self, cells, t_ns, free_in=None):
+        J, T = self.pr.n_jobs, self.pr.n_types
+        dec = np.zeros(J, np.int64)
+        fa = np.zeros(T, np.int32)
+        tot = C.c_double()
+        fi = None if free_in is None else np.ascontiguousarray(free_in, np.int32)
+        t_ns = np.ascontiguousarray(t_ns, np.int64)
+        self._check(self.L.oracle_round(C.byref(self.s), C.c_int64(len(t_ns)),
+                                        *[_ptr(cells[k]) for k in ("job", "type", "G", "S")],
+                                        _ptr(t_ns), None if fi is None else _ptr(fi), _ptr(dec),
+                                        _ptr(fa), C.byref(tot)), "round")
+        return dec, fa, tot.value
+
+
+def comm(kind, p, alpha, beta, V, n=1):
+    return lib().oracle_comm(kind, p, alpha, beta, V, n)

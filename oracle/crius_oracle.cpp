@@ -1,0 +1,484 @@
+// crius_oracle.cpp -- TEST INFRASTRUCTURE ONLY (see crius_oracle.h).
+//
+// A plain, slow, single-threaded CPU implementation of what the Crius hot path
+// computes, written from the paper (arXiv 2403.16125, /root/reference/PAPER.md,
+// cited as P:<line>) and the normative readings of SURVEY.md §8(c) / §N0-§N6
+// (cited as §Nx, A-n).  Every sum is taken directly over its layers, every
+// argmin is a first-minimum scan, the round is executed literally.  No prefix
+// sums, no binary search, no caching beyond what the definitions state.
+//
+// Arithmetic: all decision-path quantities are integers (A-1); intermediate
+// products use signed/unsigned 128-bit so nothing can wrap; any result that
+// would leave the documented range (T_iter < 2^62, §N0) returns code 7.
+// fp64 appears only in the round's scores (§N6), with no FMA contraction
+// (built with -ffp-contract=off).
+//
+// Parity pins for every function live in tests/test_oracle_pins.py.
+#include "crius_oracle.h"
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+static const int64_t INF = INT64_MAX;
+static const int64_t MIB = 1 << 20;
+static const i128 LIMIT = (i128)1 << 62;
+
+namespace {
+
+struct Overflow {};
+
+int64_t narrow(i128 v) {
+  if (v < 0 || v >= LIMIT) throw Overflow();
+  return (int64_t)v;
+}
+
+// cdiv(a, b) = ceil(a / b) for a >= 0, b > 0 (§N0).
+i128 cdiv(i128 a, i128 b) { return (a + b - 1) / b; }
+
+int ilog2(int64_t x) {
+  int e = 0;
+  while ((int64_t(1) << e) < x) ++e;
+  return e;
+}
+
+// ---- §N4 communication (A-14: ring alpha-beta; beta in ns per MiB) --------
+// AR(p, l, V, n) = 0 if p == 1 else n*2(p-1)*alpha + cdiv(2(p-1)*V*beta, p*2^20)
+i128 AR(i128 p, i128 alpha, i128 beta, i128 V, i128 n) {
+  if (p == 1) return 0;
+  return n * 2 * (p - 1) * alpha + cdiv(2 * (p - 1) * V * beta, p * MIB);
+}
+// AG(p, l, V) = 0 if p == 1 else (p-1)*alpha + cdiv((p-1)*V*beta, p*2^20)
+i128 AG(i128 p, i128 alpha, i128 beta, i128 V) {
+  if (p == 1) return 0;
+  return (p - 1) * alpha + cdiv((p - 1) * V * beta, p * MIB);
+}
+// P2P(l, V) = alpha + cdiv(V*beta, 2^20)
+i128 P2P(i128 alpha, i128 beta, i128 V) { return alpha + cdiv(V * beta, MIB); }
+
+struct Cell {
+  int32_t job, type, G, S, nplans;
+};
+
+// ---- §N2 enumeration ("Initializing Cells"; A-6) ---------------
+std::vector<int32_t> gpu_counts(const oracle_problem *pr, int j, int t) {
+  std::vector<int32_t> Gs;
+  int32_t cap = pr->cap[t], ng = pr->ng[j];
+  if (pr->gpu_set == 0) {  // paper: N_G/2, N_G, 2N_G
+    if (ng >= 2 && ng / 2 <= cap) Gs.push_back(ng / 2);
+    if (ng <= cap) Gs.push_back(ng);
+    if (2 * ng <= cap) Gs.push_back(2 * ng);
+  } else {  // all powers of two <= capacity
+    for (int32_t G = 1; G <= cap; G *= 2) Gs.push_back(G);
+  }
+  return Gs;
+}
+
+int32_t n_bvalues(const oracle_problem *pr) { return pr->b_mode == 0 ? 1 : pr->b_count; }
+
+// Bset[b]: {4S} (GPipe) or the configured list (A-11).
+int32_t b_value(const oracle_problem *pr, int32_t S, int32_t b) {
+  return pr->b_mode == 0 ? 4 * S : pr->b_values[b];
+}
+
+std::vector<Cell> enumerate(const oracle_problem *pr) {
+  std::vector<Cell> cells;
+  for (int32_t j = 0; j < pr->n_jobs; ++j)
+    for (int32_t t = 0; t < pr->n_types; ++t)
+      for (int32_t G : gpu_counts(pr, j, t))
+        for (int32_t S = 1; S <= std::min(std::min(G, pr->n_layers[j]), pr->s_max); S *= 2)
+          if (G / S <= pr->g_max) {
+            int32_t g = G / S;
+            int32_t K = ilog2(g) + 1;  // k = 0..log2 g
+            cells.push_back({j, t, G, S, K * n_bvalues(pr)});
+          }
+  return cells;
+}
+
+// ---- §N3 stage split: min-max DP over tp=1 per-layer compute (A-2..A-4) ---
+// f[1][i] = P[i];  f[s][i] = min_{k in [s-1, i-1]} max(f[s-1][k], P[i]-P[k]);
+// a[s][i] = smallest k attaining it (strict < while scanning k ascending);
+// b_S = L, b_{s-1} = a[s][b_s].
+std::vector<int32_t> split(const oracle_problem *pr, int32_t j, int32_t t, int32_t S) {
+  const int32_t L = pr->n_layers[j];
+  const int64_t off = pr->layer_off[j];
+  const int64_t TL = pr->layer_off[pr->n_jobs];
+  const int32_t *c0 = pr->c + ((int64_t)t * (pr->k_max + 1) + 0) * TL + off;
+  std::vector<std::vector<int64_t>> f(S + 1, std::vector<int64_t>(L + 1, INF));
+  std::vector<std::vector<int32_t>> arg(S + 1, std::vector<int32_t>(L + 1, -1));
+  std::vector<int64_t> last(L + 1, 0);  // last[k] = cost of the stage [k, i)
+  for (int32_t i = 1; i <= L; ++i) {
+    f[1][i] = 0;
+    for (int32_t l = 0; l < i; ++l) f[1][i] += c0[l];
+  }
+  for (int32_t s = 2; s <= S; ++s)
+    for (int32_t i = s; i <= L; ++i) {
+      // the stage [k, i) summed directly over its layers, k = i-1 down to 0
+      last[i] = 0;
+      for (int32_t k = i - 1; k >= 0; --k) last[k] = last[k + 1] + c0[k];
+      for (int32_t k = s - 1; k <= i - 1; ++k) {
+        int64_t v = std::max(f[s - 1][k], last[k]);
+        if (v < f[s][i]) {
+          f[s][i] = v;
+          arg[s][i] = k;
+        }
+      }
+    }
+  std::vector<int32_t> b(S + 1);
+  b[S] = L;
+  for (int32_t s = S; s >= 2; --s) b[s - 1] = arg[s][b[s]];
+  b[0] = 0;
+  return b;
+}
+
+// ---- §N5 plan cost, every stage sum taken directly over its layers -------
+struct PlanOut {
+  bool feasible;
+  int64_t t_iter;
+};
+
+PlanOut plan_cost(const oracle_problem *pr, const Cell &cell, const std::vector<int32_t> &b,
+                  int32_t p, int64_t *T_out, int64_t *sync_out, int64_t *mem_out) {
+  const int32_t j = cell.job, t = cell.type, S = cell.S;
+  const int64_t off = pr->layer_off[j];
+  const int64_t TL = pr->layer_off[pr->n_jobs];
+  const int32_t nB = n_bvalues(pr);
+  const int32_t k = p / nB;                      // plan p = k*nB + b (A-9)
+  const int32_t B = b_value(pr, S, p % nB);
+  const i128 g = cell.G / S;                     // uniform GPUs per stage (A-5)
+  const i128 tp = (i128)1 << k, dp = g / tp;
+  const i128 GB = pr->gb[j];
+  if (B * dp > GB) return {false, 0};            // A-12
+  const i128 mb = GB / (B * dp);
+  const int64_t gpn = pr->gpn[t];
+  const int32_t *ck = pr->c + ((int64_t)t * (pr->k_max + 1) + k) * TL + off;
+  // link classes (A-15)
+  const bool tp_in = tp <= gpn, dp_in = g <= gpn;
+  const i128 a_tp = tp_in ? pr->alpha_in[t] : pr->alpha_x[t];
+  const i128 b_tp = tp_in ? pr->beta_in[t] : pr->beta_x[t];
+  const i128 a_dp = dp_in ? pr->alpha_in[t] : pr->alpha_x[t];
+  const i128 b_dp = dp_in ? pr->beta_in[t] : pr->beta_x[t];
+  bool feasible = true;
+  i128 sumT = 0, maxT = 0, maxSync = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    const int32_t a = b[s], e = b[s + 1];
+    i128 C = 0, TPV = 0, TPN = 0, W = 0, A = 0;
+    for (int32_t l = a; l < e; ++l) {
+      C += ck[l];
+      TPV += pr->tpv[off + l];
+      TPN += pr->tpn[off + l];
+      W += pr->w[off + l];
+      A += pr->act[off + l];
+    }
+    const i128 comp = mb * C;
+    const i128 tpc = AR(tp, a_tp, b_tp, mb * TPV, TPN);
+    i128 inb = 0;
+    if (s > 0) {
+      const bool b_in = (g < gpn) && ((int64_t)s % (gpn / (int64_t)g) != 0);
+      const i128 a_b = b_in ? pr->alpha_in[t] : pr->alpha_x[t];
+      const i128 b_b = b_in ? pr->beta_in[t] : pr->beta_x[t];
+      const i128 V = mb * pr->bnd[off + a - 1];
+      inb = P2P(a_b, b_b, cdiv(V, tp)) + AG(tp, a_tp, b_tp, V);
+    }
+    const i128 T = comp + tpc + inb;
+    const i128 sync = AR(dp, a_dp, b_dp, cdiv(W, tp), 1);
+    const i128 mem = cdiv((i128)pr->kst[j] * W + (GB / dp) * A, tp);
+    if (mem > pr->mem[t]) feasible = false;       // memory filter (A-13)
+    if (T_out) T_out[s] = narrow(T);
+    if (sync_out) sync_out[s] = narrow(sync);
+    if (mem_out) mem_out[s] = narrow(mem);
+    sumT += T;
+    maxT = std::max(maxT, T);
+    maxSync = std::max(maxSync, sync);
+  }
+  // T_iter = sum_s T_s + (B-1) max_s T_s + max_s sync_s   (north_star; D4, A-7)
+  const i128 t_iter = sumT + (i128)(B - 1) * maxT + maxSync;
+  return {feasible, narrow(t_iter)};
+}
+
+bool valid_problem(const oracle_problem *pr) {
+  if (!pr || pr->n_types < 1 || pr->n_jobs < 0 || pr->k_max < 0) return false;
+  if (pr->s_max < 1 || pr->g_max < 1 || pr->g_max > (1 << pr->k_max) || pr->depth < 0) return false;
+  if (pr->b_mode == 1 && pr->b_count < 1) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t oracle_comm(int32_t kind, int64_t p, int64_t alpha, int64_t beta, int64_t V, int64_t n) {
+  if (kind == 0) return (int64_t)AR(p, alpha, beta, V, n);
+  if (kind == 1) return (int64_t)AG(p, alpha, beta, V);
+  return (int64_t)P2P(alpha, beta, V);
+}
+
+int oracle_count(const oracle_problem *pr, int64_t *n_cells, int64_t *n_plans) {
+  if (!valid_problem(pr)) return 2;
+  std::vector<Cell> cells = enumerate(pr);
+  int64_t np = 0;
+  for (const Cell &c : cells) np += c.nplans;
+  *n_cells = (int64_t)cells.size();
+  *n_plans = np;
+  return 0;
+}
+
+int oracle_enumerate(const oracle_problem *pr, int32_t *cell_job, int32_t *cell_type,
+                     int32_t *cell_G, int32_t *cell_S, int32_t *cell_nplans) {
+  if (!valid_problem(pr)) return 2;
+  std::vector<Cell> cells = enumerate(pr);
+  for (size_t i = 0; i < cells.size(); ++i) {
+    cell_job[i] = cells[i].job;
+    cell_type[i] = cells[i].type;
+    cell_G[i] = cells[i].G;
+    cell_S[i] = cells[i].S;
+    cell_nplans[i] = cells[i].nplans;
+  }
+  return 0;
+}
+
+int oracle_split(const oracle_problem *pr, int32_t j, int32_t t, int32_t S, int32_t *bounds) {
+  if (!valid_problem(pr) || j < 0 || j >= pr->n_jobs || t < 0 || t >= pr->n_types) return 2;
+  if (S < 1 || S > pr->n_layers[j]) return 2;
+  std::vector<int32_t> b = split(pr, j, t, S);
+  for (int32_t s = 0; s <= S; ++s) bounds[s] = b[s];
+  return 0;
+}
+
+int oracle_plan_cost(const oracle_problem *pr, int32_t j, int32_t t, int32_t G, int32_t S,
+                     int32_t p, int64_t *T_stage, int64_t *sync_stage, int64_t *mem_stage,
+                     int64_t *t_iter, int32_t *feasible) {
+  if (!valid_problem(pr) || j < 0 || j >= pr->n_jobs || t < 0 || t >= pr->n_types) return 2;
+  if (S < 1 || S > pr->n_layers[j] || G < S || G % S) return 2;
+  Cell cell{j, t, G, S, (ilog2(G / S) + 1) * n_bvalues(pr)};
+  if (p < 0 || p >= cell.nplans) return 2;
+  try {
+    std::vector<int32_t> b = split(pr, j, t, S);
+    PlanOut o = plan_cost(pr, cell, b, p, T_stage, sync_stage, mem_stage);
+    *feasible = o.feasible ? 1 : 0;
+    *t_iter = o.feasible ? o.t_iter : INF;
+  } catch (Overflow &) {
+    return 7;
+  }
+  return 0;
+}
+
+int oracle_estimate(const oracle_problem *pr, const int32_t *cell_job, const int32_t *cell_type,
+                    const int32_t *cell_G, const int32_t *cell_S, const int32_t *cell_nplans,
+                    int64_t c0, int64_t c1, int64_t *t_ns, int32_t *plan) {
+  if (!valid_problem(pr) || c0 < 0 || c1 < c0) return 2;
+  try {
+    // memo of O2 results for the current (job, type): splits do not depend on G
+    int32_t memo_j = -1, memo_t = -1;
+    std::vector<std::vector<int32_t>> memo;
+    for (int64_t i = c0; i < c1; ++i) {
+      Cell cell{cell_job[i], cell_type[i], cell_G[i], cell_S[i], cell_nplans[i]};
+      if (cell.job != memo_j || cell.type != memo_t) {
+        memo_j = cell.job;
+        memo_t = cell.type;
+        memo.assign(pr->n_layers[cell.job] + 1, std::vector<int32_t>());
+      }
+      if (memo[cell.S].empty()) memo[cell.S] = split(pr, cell.job, cell.type, cell.S);
+      const std::vector<int32_t> &b = memo[cell.S];
+      // O4: first minimum over p ascending, strict < (lowest p wins ties, A-10)
+      int64_t best = INF;
+      int32_t best_p = -1;
+      for (int32_t p = 0; p < cell.nplans; ++p) {
+        PlanOut o = plan_cost(pr, cell, b, p, nullptr, nullptr, nullptr);
+        if (o.feasible && o.t_iter < best) {
+          best = o.t_iter;
+          best_p = p;
+        }
+      }
+      t_ns[i - c0] = best;
+      plan[i - c0] = best_p;
+    }
+  } catch (Overflow &) {
+    return 7;
+  }
+  return 0;
+}
+
+// ---- §N6 scheduling round (Alg. 1; policy P:466-507) ----------
+int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,
+                 const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                 const int64_t *t_ns, const int32_t *free_in, int64_t *decision,
+                 int32_t *free_after, double *total_score) {
+  if (!valid_problem(pr) || n_cells < 0) return 2;
+  const int32_t J = pr->n_jobs, TT = pr->n_types, d = pr->depth;
+
+  // Options O_j: for each (t, G) with a feasible Cell, the Cell with min (T_c, S_c),
+  // listed in (t, G) ascending order.
+  struct Opt {
+    int32_t t, G;
+    int64_t T, cell;
+    int32_t S;
+  };
+  std::vector<std::vector<Opt>> O(J);
+  std::vector<int64_t> ref(J, INF);
+  std::vector<int64_t> ref_any(J, INF);
+  for (int64_t c = 0; c < n_cells; ++c) {
+    const int32_t j = cell_job[c];
+    if (t_ns[c] == INF) continue;
+    ref_any[j] = std::min(ref_any[j], t_ns[c]);
+    if (cell_G[c] == pr->ng[j]) ref[j] = std::min(ref[j], t_ns[c]);
+    bool found = false;
+    for (Opt &o : O[j])
+      if (o.t == cell_type[c] && o.G == cell_G[c]) {
+        found = true;
+        if (t_ns[c] < o.T || (t_ns[c] == o.T && cell_S[c] < o.S)) o = {o.t, o.G, t_ns[c], c, cell_S[c]};
+      }
+    if (!found) O[j].push_back({cell_type[c], cell_G[c], t_ns[c], c, cell_S[c]});
+  }
+  for (int32_t j = 0; j < J; ++j) {
+    std::sort(O[j].begin(), O[j].end(),
+              [](const Opt &a, const Opt &b) { return a.t != b.t ? a.t < b.t : a.G < b.G; });
+    if (ref[j] == INF) ref[j] = ref_any[j];  // else best overall; INF -> unschedulable
+  }
+  auto score = [&](int32_t j, const Opt &o) { return (double)ref[j] / (double)o.T; };
+  // kappa(o) = (T_o, G_o, t_o) ascending
+  auto kappa_less = [](const Opt &a, const Opt &b) {
+    if (a.T != b.T) return a.T < b.T;
+    if (a.G != b.G) return a.G < b.G;
+    return a.t < b.t;
+  };
+
+  // pi = jobs by (submit, id) ascending (A-18)
+  std::vector<int32_t> pi(J);
+  for (int32_t j = 0; j < J; ++j) pi[j] = j;
+  std::sort(pi.begin(), pi.end(), [&](int32_t a, int32_t b) {
+    if (pr->submit[a] != pr->submit[b]) return pr->submit[a] < pr->submit[b];
+    return pr->job_id[a] < pr->job_id[b];
+  });
+
+  std::vector<int32_t> fr(TT);
+  for (int32_t t = 0; t < TT; ++t) fr[t] = free_in ? free_in[t] : pr->cap[t];
+  std::vector<int32_t> cur(J, -1);  // index into O[j]; -1 = not admitted
+
+  // ScaleResource(j) (A-17): at most d victim moves per option trial.
+  struct Move {
+    int32_t v, o2;
+    double loss;
+  };
+  auto scale_resource = [&](int32_t j) -> bool {
+    std::vector<int32_t> opts;
+    for (int32_t i = 0; i < (int32_t)O[j].size(); ++i)
+      if (O[j][i].G <= pr->ng[j]) opts.push_back(i);
+    std::sort(opts.begin(), opts.end(),
+              [&](int32_t a, int32_t b) { return kappa_less(O[j][a], O[j][b]); });
+    for (int32_t oi : opts) {
+      const Opt &o = O[j][oi];
+      std::vector<int32_t> fr2 = fr;
+      std::vector<Move> moves;
+      while (o.G > fr2[o.t] && (int32_t)moves.size() < d) {
+        bool have = false;
+        double best_key = 0;
+        int32_t bv = -1, bo = -1, b_freed = 0;
+        bool b_other = false;
+        for (int32_t v : pi) {  // candidates in pi order, then o' in (t, G) order
+          if (cur[v] < 0) continue;
+          bool moved = false;
+          for (const Move &m : moves) moved = moved || m.v == v;
+          if (moved) continue;
+          const Opt &cv = O[v][cur[v]];
+          if (cv.t != o.t) continue;
+          for (int32_t i2 = 0; i2 < (int32_t)O[v].size(); ++i2) {
+            if (i2 == cur[v]) continue;
+            const Opt &o2 = O[v][i2];
+            int32_t freed;
+            bool other;
+            if (o2.t == o.t && o2.G < cv.G) {
+              freed = cv.G - o2.G;
+              other = false;
+            } else if (o2.t != o.t && o2.G <= fr2[o2.t]) {
+              freed = cv.G;
+              other = true;
+            } else {
+              continue;
+            }
+            const double loss = score(v, cv) - score(v, o2);
+            const double key = loss / (double)freed;
+            if (!have || key < best_key) {  // first minimum: earlier pi, then (t, G)
+              have = true;
+              best_key = key;
+              bv = v;
+              bo = i2;
+              b_freed = freed;
+              b_other = other;
+            }
+          }
+        }
+        if (!have) break;
+        fr2[o.t] += b_freed;
+        if (b_other) fr2[O[bv][bo].t] -= O[bv][bo].G;
+        moves.push_back({bv, bo, score(bv, O[bv][cur[bv]]) - score(bv, O[bv][bo])});
+      }
+      if (o.G <= fr2[o.t]) {
+        double acc = 0.0;
+        for (const Move &m : moves) acc = acc + m.loss;
+        if (score(j, o) > acc) {
+          for (const Move &m : moves) cur[m.v] = m.o2;
+          cur[j] = oi;
+          fr = fr2;
+          fr[o.t] -= o.G;
+          return true;
+        }
+      }
+    }
+    return false;
+  };
+
+  // Phase A: SchedArrival
+  for (int32_t j : pi) {
+    if (ref[j] == INF) continue;  // unschedulable
+    int32_t best = -1;
+    for (int32_t i = 0; i < (int32_t)O[j].size(); ++i) {
+      const Opt &o = O[j][i];
+      if (o.G <= pr->ng[j] && o.G <= fr[o.t] && (best < 0 || kappa_less(o, O[j][best]))) best = i;
+    }
+    if (best >= 0) {
+      cur[j] = best;
+      fr[O[j][best].t] -= O[j][best].G;
+    } else if (d >= 1 && scale_resource(j)) {
+      // admitted by resource scaling
+    }
+  }
+
+  // Phase B: extra scheduling / reverse scaling, <= d sweeps
+  for (int32_t sweep = 0; sweep < d; ++sweep) {
+    bool changed = false;
+    for (int32_t j : pi) {
+      if (cur[j] < 0) continue;
+      const Opt cj = O[j][cur[j]];
+      int32_t best = -1;
+      for (int32_t i = 0; i < (int32_t)O[j].size(); ++i) {
+        if (i == cur[j]) continue;
+        const Opt &o = O[j][i];
+        const int32_t avail = fr[o.t] + (o.t == cj.t ? cj.G : 0);
+        if (o.G <= avail && o.T < cj.T && (best < 0 || kappa_less(o, O[j][best]))) best = i;
+      }
+      if (best >= 0) {
+        fr[cj.t] += cj.G;
+        fr[O[j][best].t] -= O[j][best].G;
+        cur[j] = best;
+        changed = true;
+      }
+    }
+    if (!changed) break;
+  }
+
+  double total = 0.0;
+  for (int32_t j : pi)
+    if (cur[j] >= 0) total = total + score(j, O[j][cur[j]]);
+  for (int32_t j = 0; j < J; ++j)
+    decision[j] = ref[j] == INF ? -2 : (cur[j] < 0 ? -1 : O[j][cur[j]].cell);
+  for (int32_t t = 0; t < TT; ++t) free_after[t] = fr[t];
+  *total_score = total;
+  return 0;
+}
+
+}  // extern "C"
