@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py -- Crius hot path on B200: full-space Cell estimation + one round.
+
+One "step" = one pass of the whole hot path over the synthetic
+workload with profiles resident in HBM: enumerate every Cell (K1), estimate
+every Cell (fused DP + plan cost + argmin), all-gather the per-Cell records
+(N > 1, NCCL), and one scheduling round (K5/K6) with decisions read back.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl crius|reference]
+
+Default workload: BASELINE.json configs[3] (the north_star target: 10k-job
+Philly-like trace, 4 GPU types x 512 = 2048 GPUs, stages 1-16, DP x TP <= 64).
+Prints ONE JSON line on rank 0.  `value` = Cell-plan evaluations per second of
+the whole step (sum of plans of all Cells / step time), aggregated over all
+ranks (strong scaling: the Cell space is fixed and sharded).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2403_16125_b200 import workload as W  # noqa: E402
+
+ALU_OPS_PER_DP_PROBE = 8      # one binary-search probe of the stage DP
+ALU_OPS_PER_STAGE_EVAL = 40   # one (plan, stage) cost evaluation
+SM_COUNT = 148
+INT_LANES_PER_SM = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="crius", choices=["crius", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+def workload_name(a):
+    v = f"-{a.variant}" if a.variant else ""
+    s = f"x{a.scale}" if a.scale != 1 else ""
+    return f"cfg{a.config}{v}{s}"
+
+
+def config_dict(a, pr, n_cells, n_plans, world, flush):
+    return {"workload": workload_name(a), "jobs": pr.n_jobs, "gpu_types": pr.n_types,
+            "cluster_gpus": int(pr.cap.sum()), "cells": int(n_cells), "cell_plans": int(n_plans),
+            "gpu_set": ["paper3", "all_pow2"][pr.gpu_set], "s_max": pr.s_max, "g_max": pr.g_max,
+            "microbatches": "4S" if pr.b_mode == 0 else [int(b) for b in pr.b_values],
+            "search_depth": pr.depth, "parallelism": f"cell-range sharding x{world} + all-gather",
+            "l2": "flushed between steps (256 MiB write)" if flush else "not flushed"}
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.1)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- helpers
+def algorithmic_ops(pr, cells, units):
+    """DP probes S_top*L*ceil(log2 L) per unit + stage evaluations
+    sum(nplans * S) per Cell, for the Cells of the given unit set."""
+    job, S, npl = cells["job"], cells["S"], cells["nplans"]
+    stage_evals = int((npl.astype(np.int64) * S).sum())
+    unit = job.astype(np.int64) * pr.n_types + cells["type"]
+    stop = np.zeros(units, np.int64)
+    np.maximum.at(stop, unit, S)
+    L = np.repeat(pr.n_layers.astype(np.int64), pr.n_types)
+    lg = np.maximum(1, np.ceil(np.log2(np.maximum(L, 2)))).astype(np.int64)
+    probes = int((stop * L * lg).sum())
+    return probes, stage_evals, ALU_OPS_PER_DP_PROBE * probes + ALU_OPS_PER_STAGE_EVAL * stage_evals
+
+
+def unique_bytes(pr, n_cells):
+    """HBM bytes the estimate must move once: profile rows read + 16 B per Cell written."""
+    K1e = pr.k_max + 1
+    return int(pr.n_types * K1e * pr.total_layers * 4 + pr.total_layers * (8 * 5 + 4)
+               + n_cells * (4 * 5 + 8) + n_cells * 16)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def committed_traffic(name):
+    p = os.path.join(ROOT, "profiles", "estimate_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(name)
+    return None
+
+
+# --------------------------------------------------------------- reference arm (oracle)
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    pr = W.make_config(a.config, variant=a.variant, scale=a.scale)
+    o = oracle.Oracle(pr)
+    cells = o.enumerate()
+    n, p = o.count()
+    # bounded sample: whole-space estimate of the first units covering <= ~2.5 s of CPU work
+    c1 = len(cells["job"])
+    t0 = time.perf_counter()
+    o.estimate(cells, 0, min(c1, 2000))
+    per_cell = (time.perf_counter() - t0) / min(c1, 2000)
+    c1 = int(min(c1, max(2000, 2.5 / max(per_cell, 1e-9))))
+    sample_plans = int(cells["nplans"][:c1].sum())
+    full = c1 == len(cells["job"])
+    times = []
+    for i in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        t_ns, _ = o.estimate(cells, 0, c1)
+        if full:
+            o.round(cells, t_ns)
+        dt = time.perf_counter() - t0
+        if i >= a.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = sample_plans * a.steps / tot
+    sample = (f"full workload ({n} Cells, {p} plans) estimate + round" if full else
+              f"first {c1} of {n} Cells ({sample_plans} plans), estimate only")
+    line = {"metric": "Cell-plan evaluations/sec", "value": value, "unit": "cell-plans/s",
+            "impl": "reference", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded)",
+            "config": config_dict(a, pr, n, p, world, False),
+            "cpu_baseline": {"value": value, "unit": "cell-plans/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "cell-plans/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(a, pr):
+    """The oracle as it stands on this host, one core, bounded sample (~10-30 s)."""
+    import oracle
+    oracle.build()
+    o = oracle.Oracle(pr)
+    cells = o.enumerate()
+    n = len(cells["job"])
+    t0 = time.perf_counter()
+    c1 = min(n, 2000)
+    o.estimate(cells, 0, c1)
+    dt = time.perf_counter() - t0
+    budget = 12.0
+    if n > c1 and dt * n / c1 > budget:  # estimate a prefix of the Cell space only
+        c1 = int(min(n, max(c1, budget * c1 / max(dt, 1e-9))))
+        t0 = time.perf_counter()
+        o.estimate(cells, 0, c1)
+        dt = time.perf_counter() - t0
+        plans = int(cells["nplans"][:c1].sum())
+        return {"value": plans / dt, "unit": "cell-plans/s", "cores": 1, "kind": "oracle",
+                "sample": f"estimate of the first {c1} of {n} Cells ({plans} plans), no round"}
+    t0 = time.perf_counter()
+    t_ns, _ = o.estimate(cells)
+    t1 = time.perf_counter()
+    o.round(cells, t_ns)
+    t2 = time.perf_counter()
+    plans = int(cells["nplans"].sum())
+    return {"value": plans / (t2 - t0), "unit": "cell-plans/s", "cores": 1, "kind": "oracle",
+            "sample": f"full workload: estimate {t1 - t0:.2f} s + round {t2 - t1:.2f} s",
+            "estimate_s": t1 - t0, "round_s": t2 - t1}
+
+
+# --------------------------------------------------------------- our arm
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2403_16125_b200 as pkg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+
+    pr = W.make_config(a.config, variant=a.variant, scale=a.scale)
+    cr = pkg.Crius(pr, device=local)
+    n_cells, n_plans, n_units = cr.enumerate()
+    ub, cb = cr.partition(world)
+    chunk = int(max(cb[r + 1] - cb[r] for r in range(world)))
+    mine = cr.new_results(chunk)
+    gathered = cr.new_results(world * chunk) if world > 1 else None
+    full = cr.new_results(n_cells)
+    cells_h = {k: v.cpu().numpy() for k, v in cr.cells().items()}
+    flush = not a.no_flush
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(times=None):
+        e0, e1, e2, e3, e4 = ev(), ev(), ev(), ev(), ev()
+        e0.record(stream)
+        cr.enumerate()
+        if world > 1:
+            cr.partition(world)
+        e1.record(stream)
+        cr.estimate(ub[rank], ub[rank + 1], out=mine)
+        e2.record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, mine)
+            res = cr.compact(gathered, chunk, world, cb, out=full)
+        else:
+            res = mine
+        e3.record(stream)
+        dec = cr.schedule_round(res)
+        e4.record(stream)
+        if times is not None:
+            times.append((e0, e1, e2, e3, e4))
+        return dec
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = cr.launches()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(a.steps):
+            if flush:
+                flush_buf.fill_(1)
+            step(times)
+        torch.cuda.synchronize()
+    launches = cr.launches() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    seg = np.array([[t[i].elapsed_time(t[i + 1]) for i in range(4)] for t in times])  # ms
+    step_ms = seg.sum(axis=1)
+    tot_ms = float(step_ms.sum())
+    tot_t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot_t, op=dist.ReduceOp.MAX)
+    tot_ms = float(tot_t.item())
+    ms_per_step = tot_ms / a.steps
+    value = n_plans * a.steps / (tot_ms / 1e3)
+    est_ms = float(np.median(seg[:, 1]))
+
+    # estimate-kernel roofline (ALU-bound; HBM fraction reported beside it)
+    probes, stage_evals, ops = algorithmic_ops(pr, cells_h, n_units)
+    r_units = int(ub[rank + 1] - ub[rank])
+    frac_units = r_units / max(n_units, 1)
+    peaks, src = load_peaks()
+    clocks = clk.summary()
+    peak_ops = SM_COUNT * INT_LANES_PER_SM * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    achieved_ops = ops * frac_units / (est_ms / 1e3)
+    hbm = unique_bytes(pr, n_cells) * frac_units / (est_ms / 1e3) / 1e9
+
+    # e2e through the public API: pinned host inputs -> update (H2D) -> enumerate
+    # -> estimate -> round (decisions D2H), same metric
+    e2e = None
+    if not a.no_e2e and world == 1:
+        pin = {}
+        for k in ("c", "w", "act", "bnd", "tpv", "tpn", "job_id", "submit", "ng", "gb", "kst",
+                  "n_layers", "layer_off", "cap", "gpn", "mem", "alpha_in", "beta_in", "alpha_x",
+                  "beta_x"):
+            arr = np.ascontiguousarray(getattr(pr, k))
+            tt = torch.from_numpy(arr).pin_memory()
+            pin[k] = tt
+            setattr(pr, k, tt.numpy())
+        h2d = sum(int(t.numel() * t.element_size()) for t in pin.values())
+        d2h = pr.n_jobs * 8 + pr.n_types * 4 + 8 + 3 * 8 + (pr.n_jobs + 1) * 4
+        for _ in range(a.warmup):
+            cr.update(pr)
+            cr.enumerate()
+            cr.schedule_round(cr.estimate(out=mine))
+        torch.cuda.synchronize()
+        es, ee = ev(), ev()
+        es.record(stream)
+        for _ in range(a.steps):
+            cr.update(pr)
+            cr.enumerate()
+            cr.schedule_round(cr.estimate(out=mine))
+        ee.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = es.elapsed_time(ee) / a.steps
+        e2e = {"value": n_plans / (e2e_ms / 1e3), "unit": "cell-plans/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+
+    line = {"metric": "Cell-plan evaluations/sec", "value": value, "unit": "cell-plans/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded generator, paper-shaped workloads)",
+            "config": config_dict(a, pr, n_cells, n_plans, world, flush),
+            "breakdown_ms": {"enumerate": float(np.median(seg[:, 0])), "estimate": est_ms,
+                             "gather": float(np.median(seg[:, 2])),
+                             "round": float(np.median(seg[:, 3]))},
+            "estimate_evals_per_s": n_plans * frac_units / (est_ms / 1e3),
+            "roofline": {"kernel": "k_estimate", "bound": "alu", "achieved": achieved_ops / 1e12,
+                         "peak": peak_ops / 1e12, "unit": "Tops/s",
+                         "frac": achieved_ops / peak_ops,
+                         "traffic": committed_traffic(workload_name(a)),
+                         "peak_source": f"{SM_COUNT} SMs x {INT_LANES_PER_SM} int lanes x "
+                                        f"sm_max_mhz ({src})",
+                         "ops_per_launch": ops * frac_units, "dp_probes": probes,
+                         "stage_evals": stage_evals,
+                         "hbm_gbs": hbm, "hbm_frac": hbm / float(peaks.get("hbm_gbs", 6650.0))},
+            "clocks": clocks, "gpu_launches": int(launches)}
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and not a.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(a, W.make_config(a.config, variant=a.variant,
+                                                             scale=a.scale))
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if a.json_out:
+            with open(a.json_out, "w") as f:
+                f.write(s + "\n")
+    cr.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,719 @@
+// crius_lib.cu -- libcrius: C-ABI host side (include/crius.h) + kernel launches.
+//
+// Host code here only validates, allocates, copies and launches; every step of
+// the hot path runs in the kernels of enumerate.cuh, estimate.cuh, round.cuh.
+// There is no CPU fallback: without a CUDA device every call fails loudly.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/crius.h"
+#include "common.cuh"
+#include "enumerate.cuh"
+#include "estimate.cuh"
+#include "round.cuh"
+
+using namespace crius;
+
+namespace {
+
+thread_local std::string g_err;
+
+crius_status fail(crius_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? CRIUS_ENOMEM : CRIUS_ECUDA,         \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+  } while (0)
+
+#define CKL()                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess) return fail(CRIUS_ECUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+bool pow2(int64_t x) { return x >= 1 && (x & (x - 1)) == 0; }
+int ilog2_host(int64_t x) {
+  int e = 0;
+  while ((int64_t(1) << e) < x) ++e;
+  return e;
+}
+
+template <typename T>
+cudaError_t dalloc(T **p, size_t n) {
+  return cudaMalloc((void **)p, (n ? n : 1) * sizeof(T));
+}
+
+}  // namespace
+
+struct crius_ctx {
+  int device = 0;
+  int n_sm = 148;
+  Params P{};                 // host copy holding device pointers
+  int32_t k_max = 0;
+  int64_t TL = 0;
+  int32_t Lmax = 0;
+  int64_t launches = 0;
+  // inputs (device)
+  int32_t *d_ng = nullptr, *d_gb = nullptr, *d_kst = nullptr, *d_L = nullptr;
+  int64_t *d_off = nullptr, *d_submit = nullptr, *d_id = nullptr;
+  int32_t *d_c = nullptr, *d_tpn = nullptr;
+  int64_t *d_w = nullptr, *d_act = nullptr, *d_bnd = nullptr, *d_tpv = nullptr;
+  int32_t *d_rank = nullptr, *d_pi = nullptr;
+  int32_t *d_scratch = nullptr;  // [J + 8] stats
+  // host copies needed later
+  std::vector<int32_t> cap;
+  // enumeration
+  bool enumerated = false;
+  int64_t n_units = 0, n_cells = 0, n_plans = 0, cells_capacity = 0;
+  int32_t stat_maxcells = 0, stat_smax = 0, stat_gmax = 0;
+  Cells C{};
+  int64_t *d_scan_sums[3] = {nullptr, nullptr, nullptr};
+  int64_t scan_sums_cap = 0;
+  int64_t *d_part = nullptr;  // partition outputs
+  int32_t *d_counter = nullptr;
+  // round
+  int32_t maxopt = 0;
+  OptRec *d_opt = nullptr;
+  int64_t *d_opt_cell = nullptr, *d_ref = nullptr, *d_decision = nullptr;
+  int32_t *d_nopt = nullptr, *d_rng = nullptr, *d_cur = nullptr, *d_adm = nullptr, *d_free = nullptr;
+  double *d_total = nullptr;
+};
+
+namespace {
+
+void free_all(crius_ctx *c) {
+  void *ptrs[] = {c->d_ng, c->d_gb, c->d_kst, c->d_L, c->d_off, c->d_submit, c->d_id, c->d_c,
+                  c->d_tpn, c->d_w, c->d_act, c->d_bnd, c->d_tpv, c->d_rank, c->d_pi,
+                  c->d_scratch, c->C.job, c->C.type, c->C.G, c->C.S, c->C.nplans, c->C.plan_off,
+                  c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight,
+                  c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
+                  c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
+                  c->d_rng, c->d_cur, c->d_adm, c->d_free, c->d_total};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+}
+
+// ---- validation (host): shapes, powers of two, §N0 bounds -----------------
+struct JobSums {
+  std::vector<__int128> W, A, TPV, TPN, BNDmax;
+};
+
+crius_status validate_static(const crius_cluster *cl, const crius_jobs *jb, const crius_config *cf,
+                             int64_t *TL_out, int32_t *Lmax_out) {
+  if (!cl || !jb || !cf) return fail(CRIUS_EINVAL, "null argument");
+  if (cl->n_types < 1 || cl->n_types > kMaxTypes) return fail(CRIUS_EINVAL, "n_types must be 1..16");
+  if (!cl->capacity || !cl->gpus_per_node || !cl->mem_bytes || !cl->alpha_intra_ns ||
+      !cl->beta_intra_ns_per_mib || !cl->alpha_inter_ns || !cl->beta_inter_ns_per_mib)
+    return fail(CRIUS_EINVAL, "null cluster array");
+  for (int t = 0; t < cl->n_types; ++t) {
+    if (!pow2(cl->capacity[t]) || cl->capacity[t] > (1 << 30))
+      return fail(CRIUS_EINVAL, "capacity[" + std::to_string(t) + "] must be a power of two");
+    if (!pow2(cl->gpus_per_node[t]) || cl->gpus_per_node[t] > (1 << 30))
+      return fail(CRIUS_EINVAL, "gpus_per_node[" + std::to_string(t) + "] must be a power of two");
+    if (cl->mem_bytes[t] < 0 || cl->alpha_intra_ns[t] < 0 || cl->alpha_inter_ns[t] < 0 ||
+        cl->alpha_intra_ns[t] >= (int64_t(1) << 40) || cl->alpha_inter_ns[t] >= (int64_t(1) << 40))
+      return fail(CRIUS_EINVAL, "mem/alpha out of range for type " + std::to_string(t));
+    if (cl->beta_intra_ns_per_mib[t] < 0 || cl->beta_inter_ns_per_mib[t] < 0 ||
+        cl->beta_intra_ns_per_mib[t] >= (int64_t(1) << 40) ||
+        cl->beta_inter_ns_per_mib[t] >= (int64_t(1) << 40))
+      return fail(CRIUS_EINVAL, "beta out of range [0, 2^40) for type " + std::to_string(t));
+  }
+  if (jb->n_jobs < 1) return fail(CRIUS_EINVAL, "n_jobs must be >= 1");
+  if (jb->k_max < 0 || jb->k_max > kMaxKmax) return fail(CRIUS_EINVAL, "k_max must be 0..6");
+  if (!jb->job_id || !jb->submit_time || !jb->n_gpus_req || !jb->global_batch || !jb->k_state ||
+      !jb->n_layers || !jb->layer_off || !jb->compute_ns || !jb->param_bytes || !jb->act_bytes ||
+      !jb->boundary_bytes || !jb->tp_bytes || !jb->tp_calls)
+    return fail(CRIUS_EINVAL, "null jobs array");
+  if (jb->layer_off[0] != 0) return fail(CRIUS_EINVAL, "layer_off[0] must be 0");
+  int32_t Lmax = 0;
+  for (int j = 0; j < jb->n_jobs; ++j) {
+    const std::string js = "job " + std::to_string(j);
+    if (!pow2(jb->n_gpus_req[j]) || jb->n_gpus_req[j] > (1 << 29))
+      return fail(CRIUS_EINVAL, js + ": N_G must be a power of two");
+    if (!pow2(jb->global_batch[j]) || jb->global_batch[j] > (1 << 30))
+      return fail(CRIUS_EINVAL, js + ": global batch must be a power of two");
+    if (jb->k_state[j] < 1) return fail(CRIUS_EINVAL, js + ": k_state must be >= 1");
+    if (jb->n_layers[j] < 1 || jb->n_layers[j] > 255)
+      return fail(CRIUS_EINVAL, js + ": n_layers must be 1..255");
+    if (jb->layer_off[j + 1] != jb->layer_off[j] + jb->n_layers[j])
+      return fail(CRIUS_EINVAL, js + ": layer_off is not the prefix of n_layers");
+    Lmax = std::max(Lmax, jb->n_layers[j]);
+  }
+  if (!(cf->gpu_set == 0 || cf->gpu_set == 1)) return fail(CRIUS_EINVAL, "gpu_set must be 0 or 1");
+  if (cf->s_max < 1) return fail(CRIUS_EINVAL, "s_max must be >= 1");
+  if (!pow2(cf->g_max) || cf->g_max > (1 << jb->k_max))
+    return fail(CRIUS_EINVAL, "g_max must be a power of two <= 2^k_max");
+  if (cf->b_mode == 1) {
+    if (cf->b_count < 1 || cf->b_count > kMaxB || !cf->b_values)
+      return fail(CRIUS_EINVAL, "b_count must be 1..16");
+    for (int b = 0; b < cf->b_count; ++b)
+      if (!pow2(cf->b_values[b]) || cf->b_values[b] > (1 << 30) ||
+          (b && cf->b_values[b] <= cf->b_values[b - 1]))
+        return fail(CRIUS_EINVAL, "b_values must be ascending powers of two");
+  } else if (cf->b_mode != 0) {
+    return fail(CRIUS_EINVAL, "b_mode must be 0 or 1");
+  }
+  if (cf->search_depth < 0 || cf->search_depth > kMaxDepth)
+    return fail(CRIUS_EINVAL, "search_depth must be 0..16");
+  *TL_out = jb->layer_off[jb->n_jobs];
+  *Lmax_out = Lmax;
+  return CRIUS_OK;
+}
+
+// §N0 bounds with the per-job max of c measured on the device.
+crius_status validate_bounds(const crius_cluster *cl, const crius_jobs *jb, const crius_config *cf,
+                             const std::vector<int32_t> &maxc, int32_t minc) {
+  typedef __int128 i128;
+  if (minc < 1) return fail(CRIUS_EINVAL, "compute_ns must be >= 1 everywhere");
+  const i128 LIM52 = (i128)1 << 52, LIM62 = (i128)1 << 62, LIM63 = (i128)1 << 63, MIB = 1 << 20;
+  i128 amax = 0, bmax = 0;
+  for (int t = 0; t < cl->n_types; ++t) {
+    amax = std::max<i128>(amax, std::max(cl->alpha_intra_ns[t], cl->alpha_inter_ns[t]));
+    bmax = std::max<i128>(bmax, std::max(cl->beta_intra_ns_per_mib[t], cl->beta_inter_ns_per_mib[t]));
+  }
+  const i128 p = cf->g_max;  // tp, dp <= g <= g_max
+  for (int j = 0; j < jb->n_jobs; ++j) {
+    const std::string js = "job " + std::to_string(j);
+    const int64_t o = jb->layer_off[j];
+    const i128 L = jb->n_layers[j], GB = jb->global_batch[j];
+    i128 W = 0, A = 0, V = 0, N = 0, Bm = 0;
+    for (int l = 0; l < L; ++l) {
+      const int64_t w = jb->param_bytes[o + l], a = jb->act_bytes[o + l];
+      const int64_t bd = jb->boundary_bytes[o + l], tv = jb->tp_bytes[o + l];
+      const int32_t tn = jb->tp_calls[o + l];
+      if (w < 0 || a < 0 || bd < 0 || tv < 0 || tn < 0)
+        return fail(CRIUS_EINVAL, js + ": negative per-layer value");
+      W += w;
+      A += a;
+      V += tv;
+      N += tn;
+      Bm = std::max<i128>(Bm, bd);
+    }
+    if (L * maxc[j] * GB >= LIM52) return fail(CRIUS_EINVAL, js + ": L*max(c)*GB >= 2^52");
+    if (2 * (p - 1) * GB * V >= LIM63 || p * GB * Bm >= LIM63 || 2 * (p - 1) * W >= LIM63)
+      return fail(CRIUS_EINVAL, js + ": alpha-beta numerator >= 2^63");
+    if ((i128)jb->k_state[j] * W + GB * A >= LIM62)
+      return fail(CRIUS_EINVAL, js + ": kst*sum(w) + GB*sum(act) >= 2^62");
+    const i128 comp = GB * L * maxc[j];
+    const i128 tpc = N * 2 * (p - 1) * amax + L * (2 * (p - 1) * GB * V * bmax / MIB + 1);
+    const i128 inb = L * (amax + GB * Bm * bmax / MIB + 1 + (p - 1) * amax + (p - 1) * GB * Bm * bmax / MIB + 1);
+    const i128 X = comp + tpc + inb;
+    const i128 sync = 2 * (p - 1) * amax + 2 * (p - 1) * W * bmax / MIB + 1;
+    i128 Bmax = 4 * std::min<i128>(L, cf->s_max);
+    if (cf->b_mode == 1) Bmax = cf->b_values[cf->b_count - 1];
+    if (Bmax * X + sync >= LIM62) return fail(CRIUS_EINVAL, js + ": T_iter bound >= 2^62");
+  }
+  return CRIUS_OK;
+}
+
+crius_status copy_inputs(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
+                         cudaStream_t st) {
+  const int J = jb->n_jobs, T = cl->n_types;
+  const size_t TL = (size_t)c->TL;
+  CK(cudaMemcpyAsync(c->d_ng, jb->n_gpus_req, J * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_gb, jb->global_batch, J * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_kst, jb->k_state, J * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_L, jb->n_layers, J * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_off, jb->layer_off, (J + 1) * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_submit, jb->submit_time, J * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_id, jb->job_id, J * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_c, jb->compute_ns, (size_t)T * (jb->k_max + 1) * TL * 4,
+                     cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_w, jb->param_bytes, TL * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_act, jb->act_bytes, TL * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_bnd, jb->boundary_bytes, TL * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_tpv, jb->tp_bytes, TL * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_tpn, jb->tp_calls, TL * 4, cudaMemcpyHostToDevice, st));
+  return CRIUS_OK;
+}
+
+void fill_types(crius_ctx *c, const crius_cluster *cl) {
+  c->cap.assign(cl->capacity, cl->capacity + cl->n_types);
+  for (int t = 0; t < cl->n_types; ++t) {
+    TypeParams &tp = c->P.ty[t];
+    tp.cap = cl->capacity[t];
+    tp.gpn = cl->gpus_per_node[t];
+    tp.lgpn = ilog2_host(cl->gpus_per_node[t]);
+    tp.mem = cl->mem_bytes[t];
+    tp.a_in = cl->alpha_intra_ns[t];
+    tp.b_in = cl->beta_intra_ns_per_mib[t];
+    tp.a_x = cl->alpha_inter_ns[t];
+    tp.b_x = cl->beta_inter_ns_per_mib[t];
+  }
+}
+
+// Device stats of c -> §N0 bounds; then priority ranks.  Synchronises.
+crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
+                         const crius_config *cf, cudaStream_t st) {
+  const int J = jb->n_jobs;
+  CK(cudaMemsetAsync(c->d_scratch, 0, (J + 8) * 4, st));
+  int32_t big = INT32_MAX;
+  CK(cudaMemcpyAsync(c->d_scratch + J, &big, 4, cudaMemcpyHostToDevice, st));
+  k_profile_stats<<<J, 64, 0, st>>>(c->P, c->d_scratch, c->d_scratch + J);
+  CKL();
+  k_priority_rank<<<(J + 255) / 256, 256, 0, st>>>(c->d_submit, c->d_id, J, c->d_rank, c->d_pi);
+  CKL();
+  c->launches += 2;
+  std::vector<int32_t> stats(J + 1);
+  CK(cudaMemcpyAsync(stats.data(), c->d_scratch, (J + 1) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int32_t> maxc(stats.begin(), stats.begin() + J);
+  return validate_bounds(cl, jb, cf, maxc, stats[J]);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *crius_last_error(void) { return g_err.c_str(); }
+
+int64_t crius_kernel_launches(const crius_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cl, const crius_jobs *jb,
+                                 const crius_config *cf, int32_t device, void *stream) {
+  if (!out) return fail(CRIUS_EINVAL, "null out");
+  *out = nullptr;
+  int64_t TL = 0;
+  int32_t Lmax = 0;
+  crius_status s = validate_static(cl, jb, cf, &TL, &Lmax);
+  if (s != CRIUS_OK) return s;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(CRIUS_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(CRIUS_EINVAL, "bad device ordinal");
+  CK(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+
+  crius_ctx *c = new crius_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
+  c->k_max = jb->k_max;
+  c->TL = TL;
+  c->Lmax = Lmax;
+  const int J = jb->n_jobs, T = cl->n_types;
+  Params &P = c->P;
+  P.T = T;
+  P.J = J;
+  P.K1 = jb->k_max + 1;
+  P.TL = TL;
+  P.gpu_set = cf->gpu_set;
+  P.s_max = cf->s_max;
+  P.g_max = cf->g_max;
+  P.b_mode = cf->b_mode;
+  P.nB = cf->b_mode == 0 ? 1 : cf->b_count;
+  P.depth = cf->search_depth;
+  for (int b = 0; b < (cf->b_mode == 1 ? cf->b_count : 0); ++b) P.lB[b] = ilog2_host(cf->b_values[b]);
+  fill_types(c, cl);
+  int nG = 3;
+  if (cf->gpu_set == 1) {
+    nG = 0;
+    for (int t = 0; t < T; ++t) nG = std::max(nG, ilog2_host(cl->capacity[t]) + 1);
+  }
+  c->maxopt = T * nG;
+  if (c->maxopt > 256) {
+    delete c;
+    return fail(CRIUS_EINVAL, "n_types x GPU-count choices must be <= 256");
+  }
+
+  auto cleanup = [&](crius_status st_) {
+    free_all(c);
+    delete c;
+    return st_;
+  };
+#define CKA(call)                                                                       \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return cleanup(fail(e_ == cudaErrorMemoryAllocation ? CRIUS_ENOMEM : CRIUS_ECUDA, \
+                          std::string(#call) + ": " + cudaGetErrorString(e_)));        \
+  } while (0)
+  CKA(dalloc(&c->d_ng, J));
+  CKA(dalloc(&c->d_gb, J));
+  CKA(dalloc(&c->d_kst, J));
+  CKA(dalloc(&c->d_L, J));
+  CKA(dalloc(&c->d_off, J + 1));
+  CKA(dalloc(&c->d_submit, J));
+  CKA(dalloc(&c->d_id, J));
+  CKA(dalloc(&c->d_c, (size_t)T * P.K1 * TL));
+  CKA(dalloc(&c->d_w, TL));
+  CKA(dalloc(&c->d_act, TL));
+  CKA(dalloc(&c->d_bnd, TL));
+  CKA(dalloc(&c->d_tpv, TL));
+  CKA(dalloc(&c->d_tpn, TL));
+  CKA(dalloc(&c->d_rank, J));
+  CKA(dalloc(&c->d_pi, J));
+  CKA(dalloc(&c->d_scratch, J + 8));
+  CKA(dalloc(&c->d_counter, 4));
+  CKA(dalloc(&c->d_part, 2 * 9 + 2));
+  P.ng = c->d_ng;
+  P.gb = c->d_gb;
+  P.kst = c->d_kst;
+  P.L = c->d_L;
+  P.off = c->d_off;
+  P.c = c->d_c;
+  P.w = c->d_w;
+  P.act = c->d_act;
+  P.bnd = c->d_bnd;
+  P.tpv = c->d_tpv;
+  P.tpn = c->d_tpn;
+  s = copy_inputs(c, cl, jb, st);
+  if (s != CRIUS_OK) return cleanup(s);
+  s = finish_load(c, cl, jb, cf, st);
+  if (s != CRIUS_OK) return cleanup(s);
+#undef CKA
+  *out = c;
+  return CRIUS_OK;
+}
+
+crius_status crius_update_profiles(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
+                                   void *stream) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  if (!cl || !jb || cl->n_types != c->P.T || jb->n_jobs != c->P.J || jb->k_max != c->k_max)
+    return fail(CRIUS_EINVAL, "update_profiles: shape differs from the loaded problem");
+  crius_config cf{};
+  cf.gpu_set = c->P.gpu_set;
+  cf.s_max = c->P.s_max;
+  cf.g_max = c->P.g_max;
+  cf.b_mode = c->P.b_mode;
+  std::vector<int32_t> bv;
+  for (int b = 0; b < (c->P.b_mode ? c->P.nB : 0); ++b) bv.push_back(1 << c->P.lB[b]);
+  cf.b_count = (int32_t)bv.size();
+  cf.b_values = bv.data();
+  cf.search_depth = c->P.depth;
+  int64_t TL = 0;
+  int32_t Lmax = 0;
+  crius_status s = validate_static(cl, jb, &cf, &TL, &Lmax);
+  if (s != CRIUS_OK) return s;
+  if (TL != c->TL) return fail(CRIUS_EINVAL, "update_profiles: total layers differ");
+  for (int t = 0; t < cl->n_types; ++t)
+    if (cl->capacity[t] != c->cap[t]) return fail(CRIUS_EINVAL, "update_profiles: capacity differs");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  fill_types(c, cl);
+  c->Lmax = Lmax;
+  s = copy_inputs(c, cl, jb, st);
+  if (s != CRIUS_OK) return s;
+  c->enumerated = false;
+  return finish_load(c, cl, jb, &cf, st);
+}
+
+crius_status crius_enumerate_cells(crius_ctx *c, int64_t *n_cells, int64_t *n_plans,
+                                   int64_t *n_units, void *stream) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t U = (int64_t)c->P.J * c->P.T;
+  if (c->n_units != U || !c->C.unit_cell_begin) {
+    if (c->C.unit_cell_begin) cudaFree(c->C.unit_cell_begin);
+    if (c->C.unit_plan_begin) cudaFree(c->C.unit_plan_begin);
+    if (c->C.unit_weight) cudaFree(c->C.unit_weight);
+    CK(dalloc(&c->C.unit_cell_begin, U + 1));
+    CK(dalloc(&c->C.unit_plan_begin, U + 1));
+    CK(dalloc(&c->C.unit_weight, U + 1));
+    const int64_t tiles = (U + kScanTile - 1) / kScanTile;
+    for (int q = 0; q < 3; ++q) {
+      if (c->d_scan_sums[q]) cudaFree(c->d_scan_sums[q]);
+      CK(dalloc(&c->d_scan_sums[q], tiles + 1));
+    }
+    c->n_units = U;
+  }
+  int32_t *stats = c->d_scratch + c->P.J + 1;  // 3 ints
+  CK(cudaMemsetAsync(stats, 0, 3 * 4, st));
+  UnitCounts UC{c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight, stats};
+  k_unit_count<<<(unsigned)((U + 255) / 256), 256, 0, st>>>(c->P, UC, U);
+  CKL();
+  const int64_t tiles = (U + kScanTile - 1) / kScanTile;
+  Scan3 X{{c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight}};
+  Scan3 S{{c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2]}};
+  k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, st>>>(X, U, S);
+  CKL();
+  k_scan_sums<<<1, kScanThreads, 0, st>>>(S, tiles);
+  CKL();
+  k_scan_add<<<(unsigned)((U + 255) / 256), 256, 0, st>>>(X, U, S, tiles);
+  CKL();
+  c->launches += 4;
+  int64_t tot[2];
+  int32_t hs[3];
+  CK(cudaMemcpyAsync(&tot[0], c->C.unit_cell_begin + U, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&tot[1], c->C.unit_plan_begin + U, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs, stats, 12, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  c->n_cells = tot[0];
+  c->n_plans = tot[1];
+  c->stat_maxcells = hs[0];
+  c->stat_smax = hs[1];
+  c->stat_gmax = hs[2];
+  if (c->n_cells > c->cells_capacity) {
+    int32_t **i32s[] = {&c->C.job, &c->C.type, &c->C.G, &c->C.S, &c->C.nplans};
+    for (int32_t **p : i32s) {
+      if (*p) cudaFree(*p);
+      CK(dalloc(p, c->n_cells));
+    }
+    if (c->C.plan_off) cudaFree(c->C.plan_off);
+    CK(dalloc(&c->C.plan_off, c->n_cells));
+    c->cells_capacity = c->n_cells;
+  }
+  if (c->n_cells > 0) {
+    k_unit_fill<<<(unsigned)((U + 255) / 256), 256, 0, st>>>(c->P, c->C, U);
+    CKL();
+    c->launches += 1;
+    CK(cudaStreamSynchronize(st));
+  }
+  if (n_cells) *n_cells = c->n_cells;
+  if (n_plans) *n_plans = c->n_plans;
+  if (n_units) *n_units = U;
+  c->enumerated = true;
+  if (c->n_cells == 0) return fail(CRIUS_EINFEASIBLE, "enumeration produced zero Cells");
+  return CRIUS_OK;
+}
+
+crius_status crius_cells(crius_ctx *c, crius_cell_view *v) {
+  if (!c || !v) return fail(CRIUS_EINVAL, "null argument");
+  if (!c->enumerated) return fail(CRIUS_ESTATE, "crius_cells before crius_enumerate_cells");
+  v->n_cells = c->n_cells;
+  v->n_cell_plans = c->n_plans;
+  v->n_units = c->n_units;
+  v->job = c->C.job;
+  v->type = c->C.type;
+  v->G = c->C.G;
+  v->S = c->C.S;
+  v->nplans = c->C.nplans;
+  v->plan_off = c->C.plan_off;
+  v->unit_cell_begin = c->C.unit_cell_begin;
+  v->unit_plan_begin = c->C.unit_plan_begin;
+  return CRIUS_OK;
+}
+
+int32_t crius_split_stride(const crius_ctx *c) {
+  if (!c) return 0;
+  int nsi = 0;
+  while ((1 << nsi) <= std::max(1, c->stat_smax)) ++nsi;  // S = 1 .. stat_smax
+  return (1 << nsi) - 1 + nsi;
+}
+
+}  // extern "C"
+
+namespace {
+
+__global__ void k_partition(const int64_t *__restrict__ wprefix, const int64_t *__restrict__ ucb,
+                            int64_t n_units, int32_t world, int64_t *out) {
+  const int r = threadIdx.x;
+  if (r > world) return;
+  const int64_t W = wprefix[n_units];
+  int64_t ub;
+  if (r == world) {
+    ub = n_units;
+  } else {
+    const int64_t target = (int64_t)((__int128)W * r / world);
+    int64_t lo = 0, hi = n_units;  // first u with prefix[u] >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (wprefix[mid] >= target)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    ub = r == 0 ? 0 : lo;
+  }
+  out[r] = ub;
+  out[world + 1 + r] = ucb[ub];
+}
+
+}  // namespace
+
+extern "C" {
+
+crius_status crius_partition_units(crius_ctx *c, int32_t world, int64_t *unit_begin,
+                                   int64_t *cell_begin, void *stream) {
+  if (!c || !unit_begin || !cell_begin) return fail(CRIUS_EINVAL, "null argument");
+  if (!c->enumerated) return fail(CRIUS_ESTATE, "partition before enumerate");
+  if (world < 1 || world > 8) return fail(CRIUS_EINVAL, "world must be 1..8");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  k_partition<<<1, 32, 0, st>>>(c->C.unit_weight, c->C.unit_cell_begin, c->n_units, world, c->d_part);
+  CKL();
+  c->launches += 1;
+  std::vector<int64_t> h(2 * (world + 1));
+  CK(cudaMemcpyAsync(h.data(), c->d_part, h.size() * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int r = 0; r <= world; ++r) {
+    unit_begin[r] = h[r];
+    cell_begin[r] = h[world + 1 + r];
+  }
+  return CRIUS_OK;
+}
+
+crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit_end,
+                                  crius_cell_result *d_out, int16_t *d_splits, void *stream) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  if (!c->enumerated) return fail(CRIUS_ESTATE, "estimate before enumerate");
+  if (unit_begin < 0 || unit_end > c->n_units || unit_begin > unit_end)
+    return fail(CRIUS_EINVAL, "bad unit range");
+  if (!d_out) return fail(CRIUS_EINVAL, "null d_out");
+  if (unit_begin == unit_end) return CRIUS_OK;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  EstArgs A{};
+  A.cG = c->C.G;
+  A.cS = c->C.S;
+  A.plan_off = c->C.plan_off;
+  A.ucb = c->C.unit_cell_begin;
+  A.upb = c->C.unit_plan_begin;
+  A.unit_begin = unit_begin;
+  A.unit_end = unit_end;
+  A.out = (CellResult *)d_out;
+  A.splits = d_splits;
+  A.split_stride = crius_split_stride(c);
+  A.work_counter = c->d_counter;
+  // per-warp shared-memory layout
+  const int Lp = c->Lmax + 1;
+  const int K1e = ilog2_host(std::max(1, c->stat_gmax)) + 1;
+  const int Stop = std::max(1, c->stat_smax);
+  const int maxCells = std::max(1, c->stat_maxcells);
+  int o = 0;
+  auto take = [&](int bytes) {
+    const int at = o;
+    o += (bytes + 15) & ~15;
+    return at;
+  };
+  A.Lp = Lp;
+  A.K1e = K1e;
+  A.Stop = Stop;
+  A.maxCells = maxCells;
+  A.off_PC = take(K1e * Lp * 8);
+  A.off_PW = take(Lp * 8);
+  A.off_PA = take(Lp * 8);
+  A.off_PV = take(Lp * 8);
+  A.off_PN = take(Lp * 8);
+  A.off_BND = take(Lp * 8);
+  A.off_F = take(2 * Lp * 8);
+  A.off_ARG = take((Stop + 1) * Lp);
+  A.off_BD = take(A.split_stride * 2);
+  A.off_CELL = take(3 * (maxCells + 1) * 4);
+  A.warp_bytes = o;
+  const int64_t nunits = unit_end - unit_begin;
+  CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
+  int warps = 4;
+  if (4 * A.warp_bytes > 200 * 1024) warps = 1;
+  if (A.warp_bytes > 220 * 1024) return fail(CRIUS_EINVAL, "unit too large for shared memory");
+  const size_t smem = (size_t)warps * A.warp_bytes;
+  int per_sm = 1;
+  if (warps == 4) {
+    CK(cudaFuncSetAttribute(k_estimate<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_estimate<4>, 128, smem));
+  } else {
+    CK(cudaFuncSetAttribute(k_estimate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_estimate<1>, 32, smem));
+  }
+  per_sm = std::max(per_sm, 1);
+  const int64_t want = (nunits + warps - 1) / warps;
+  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)c->n_sm * per_sm);
+  if (warps == 4)
+    k_estimate<4><<<grid, 128, smem, st>>>(c->P, A);
+  else
+    k_estimate<1><<<grid, 32, smem, st>>>(c->P, A);
+  CKL();
+  c->launches += 1;
+  return CRIUS_OK;
+}
+
+crius_status crius_compact_gathered(crius_ctx *c, const crius_cell_result *d_gathered,
+                                    int64_t chunk_stride, int32_t world, const int64_t *cell_begin,
+                                    crius_cell_result *d_all, void *stream) {
+  if (!c || !d_gathered || !cell_begin || !d_all) return fail(CRIUS_EINVAL, "null argument");
+  if (!c->enumerated) return fail(CRIUS_ESTATE, "compact before enumerate");
+  if (world < 1 || world > 8) return fail(CRIUS_EINVAL, "world must be 1..8");
+  CompactArgs A{};
+  for (int r = 0; r <= world; ++r) A.cb[r] = cell_begin[r];
+  A.world = world;
+  A.stride = chunk_stride;
+  A.n_cells = c->n_cells;
+  for (int r = 0; r < world; ++r)
+    if (A.cb[r + 1] - A.cb[r] > chunk_stride || A.cb[r + 1] < A.cb[r])
+      return fail(CRIUS_EINVAL, "chunk larger than chunk_stride");
+  if (A.cb[0] != 0 || A.cb[world] != c->n_cells) return fail(CRIUS_EINVAL, "cell_begin must span all Cells");
+  CK(cudaSetDevice(c->device));
+  k_compact<<<(unsigned)((c->n_cells + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const CellResult *)d_gathered, A, (CellResult *)d_all);
+  CKL();
+  c->launches += 1;
+  return CRIUS_OK;
+}
+
+crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
+                                  const int32_t *free_gpus, int64_t *decision, int32_t *free_after,
+                                  double *total_score, void *stream) {
+  if (!c || !d_all || !decision || !free_after || !total_score)
+    return fail(CRIUS_EINVAL, "null argument");
+  if (!c->enumerated) return fail(CRIUS_ESTATE, "round before enumerate");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int J = c->P.J, T = c->P.T;
+  if (!c->d_opt) {
+    CK(dalloc(&c->d_opt, (size_t)J * c->maxopt));
+    CK(dalloc(&c->d_opt_cell, (size_t)J * c->maxopt));
+    CK(dalloc(&c->d_ref, J));
+    CK(dalloc(&c->d_decision, J));
+    CK(dalloc(&c->d_nopt, J));
+    CK(dalloc(&c->d_rng, J));
+    CK(dalloc(&c->d_cur, J));
+    CK(dalloc(&c->d_adm, J));
+    CK(dalloc(&c->d_free, 16));
+    CK(dalloc(&c->d_total, 1));
+  }
+  std::vector<int32_t> fr(T);
+  for (int t = 0; t < T; ++t) {
+    fr[t] = free_gpus ? free_gpus[t] : c->cap[t];
+    if (fr[t] < 0) return fail(CRIUS_EINVAL, "free_gpus must be >= 0");
+  }
+  CK(cudaMemcpyAsync(c->d_free, fr.data(), T * 4, cudaMemcpyHostToDevice, st));
+  RoundBuf R{};
+  R.J = J;
+  R.T = T;
+  R.maxopt = c->maxopt;
+  R.depth = c->P.depth;
+  R.rank = c->d_rank;
+  R.pi = c->d_pi;
+  R.ng_job = c->d_ng;
+  R.opt = c->d_opt;
+  R.opt_cell = c->d_opt_cell;
+  R.nopt = c->d_nopt;
+  R.ref = c->d_ref;
+  R.ng = c->d_rng;
+  R.cur = c->d_cur;
+  R.adm = c->d_adm;
+  R.decision = c->d_decision;
+  R.free_io = c->d_free;
+  R.total = c->d_total;
+  k_round_options<<<(J + 127) / 128, 128, 0, st>>>(c->P, c->C.unit_cell_begin, c->C.type, c->C.G,
+                                                   (const CellResult *)d_all, R);
+  CKL();
+  k_round_greedy<<<1, kRoundThreads, 0, st>>>(R);
+  CKL();
+  c->launches += 2;
+  CK(cudaMemcpyAsync(decision, c->d_decision, (size_t)J * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(free_after, c->d_free, T * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(total_score, c->d_total, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return CRIUS_OK;
+}
+
+void crius_destroy(crius_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  free_all(c);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,226 @@
+// enumerate.cuh -- K1: Cell enumeration on the device (PAPER.md
+// :481-488 "Initializing Cells": G in {N_G/2, N_G, 2N_G}, S in {1,2,4,..}).
+//
+// Cells are generated per unit u = (job j, type t) = j*T + t in the order
+// (G asc, S asc); a unit's Cells are contiguous and units are in (j, t) order,
+// so Cell ids are global positions.  Three steps: per-unit closed-form counts,
+// an exclusive scan (cells, plans, work weight), and a per-unit fill.
+#pragma once
+#include "common.cuh"
+
+namespace crius {
+
+struct UnitCounts {
+  int64_t *ncells, *nplans, *weight;  // [n_units] (scanned in place into [n_units+1])
+  int32_t *stats;                     // [0] max cells/unit, [1] max S, [2] max g
+};
+
+// Per-unit counts (one thread per unit).  weight = L*min(L,s_max)*ceil(log2 L)
+// + sum_cells nplans*S: the DP probes plus the stage evaluations of the unit
+// (SURVEY §8(e)), used to balance contiguous unit ranges across ranks.
+__global__ void k_unit_count(Params P, UnitCounts U, int64_t n_units) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int j = (int)(u / P.T), t = (int)(u % P.T);
+  const int L = P.L[j];
+  const int nG = unit_num_G(P, j, t);
+  int64_t nc = 0, np = 0, wt = 0;
+  int smax = 0, gmax = 0;
+  for (int gi = 0; gi < nG; ++gi) {
+    const int G = unit_G(P, j, t, gi);
+    const int lim = min(min(G, L), P.s_max);
+    for (int S = 1; S <= lim; S <<= 1) {
+      const int g = G / S;
+      if (g > P.g_max) continue;
+      const int np_c = (ilog2_pow2(g) + 1) * P.nB;
+      nc += 1;
+      np += np_c;
+      wt += (int64_t)np_c * S;
+      smax = max(smax, S);
+      gmax = max(gmax, g);
+    }
+  }
+  if (nc > 0) {
+    int lg = 0;
+    while ((1 << lg) < L) ++lg;
+    wt += (int64_t)L * min(L, P.s_max) * max(lg, 1);
+  }
+  U.ncells[u] = nc;
+  U.nplans[u] = np;
+  U.weight[u] = wt;
+  atomicMax(&U.stats[0], (int)nc);
+  atomicMax(&U.stats[1], smax);
+  atomicMax(&U.stats[2], gmax);
+}
+
+// ---- exclusive scan of three int64 arrays, in place, n -> n+1 entries -----
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+struct Scan3 {
+  int64_t *a[3];
+};
+
+__device__ __forceinline__ void block_excl_scan3(int64_t v[3], int64_t tot[3]) {
+  __shared__ int64_t warp_sums[3][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t incl[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    incl[q] = warp_incl_scan(v[q], lane);
+    if (lane == 31) warp_sums[q][wid] = incl[q];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int nw = blockDim.x >> 5;
+      int64_t s = lane < nw ? warp_sums[q][lane] : 0;
+      s = warp_incl_scan(s, lane);
+      warp_sums[q][lane] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int64_t before = wid ? warp_sums[q][wid - 1] : 0;
+    tot[q] = warp_sums[q][(blockDim.x >> 5) - 1];
+    v[q] = before + incl[q] - v[q];
+  }
+  __syncthreads();
+}
+
+// Tile-local exclusive scan; tile totals to `sums` (length n_tiles).
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(Scan3 X, int64_t n, Scan3 sums) {
+  const int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanItems;
+  int64_t loc[3][kScanItems], v[3], tot[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    v[q] = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      loc[q][i] = base + i < n ? X.a[q][base + i] : 0;
+      v[q] += loc[q][i];
+    }
+  }
+  block_excl_scan3(v, tot);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    int64_t run = v[q];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      if (base + i < n) X.a[q][base + i] = run;
+      run += loc[q][i];
+    }
+    if (threadIdx.x == 0) sums.a[q][blockIdx.x] = tot[q];
+  }
+}
+
+// Single block: exclusive scan of the tile sums (any length), grand total to [n_tiles].
+__global__ void __launch_bounds__(kScanThreads) k_scan_sums(Scan3 S, int64_t n_tiles) {
+  int64_t carry[3] = {0, 0, 0};
+  for (int64_t b0 = 0; b0 < n_tiles; b0 += kScanThreads) {
+    const int64_t i = b0 + threadIdx.x;
+    int64_t v[3], tot[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) v[q] = i < n_tiles ? S.a[q][i] : 0;
+    block_excl_scan3(v, tot);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (i < n_tiles) S.a[q][i] = carry[q] + v[q];
+      carry[q] += tot[q];
+    }
+  }
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) S.a[q][n_tiles] = carry[q];
+}
+
+__global__ void k_scan_add(Scan3 X, int64_t n, Scan3 sums, int64_t n_tiles) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int64_t tile = i / kScanTile;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) X.a[q][i] += sums.a[q][tile];
+  }
+  if (i == 0)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) X.a[q][n] = sums.a[q][n_tiles];
+}
+
+// Fill the Cell SoA (one thread per unit; its Cells are contiguous).
+__global__ void k_unit_fill(Params P, Cells C, int64_t n_units) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int j = (int)(u / P.T), t = (int)(u % P.T);
+  const int L = P.L[j];
+  const int nG = unit_num_G(P, j, t);
+  int64_t ci = C.unit_cell_begin[u], po = C.unit_plan_begin[u];
+  for (int gi = 0; gi < nG; ++gi) {
+    const int G = unit_G(P, j, t, gi);
+    const int lim = min(min(G, L), P.s_max);
+    for (int S = 1; S <= lim; S <<= 1) {
+      const int g = G / S;
+      if (g > P.g_max) continue;
+      const int np_c = (ilog2_pow2(g) + 1) * P.nB;
+      C.job[ci] = j;
+      C.type[ci] = t;
+      C.G[ci] = G;
+      C.S[ci] = S;
+      C.nplans[ci] = np_c;
+      C.plan_off[ci] = po;
+      ++ci;
+      po += np_c;
+    }
+  }
+}
+
+// Round priority pi (A-18): rank[j] = #{i : (submit_i, id_i) < (submit_j, id_j)};
+// pi[rank[j]] = j.  Tiled all-pairs count (ids are unique -> a permutation).
+__global__ void __launch_bounds__(256) k_priority_rank(const int64_t *submit, const int64_t *id,
+                                                       int32_t J, int32_t *rank, int32_t *pi) {
+  __shared__ int64_t ss[256], si[256];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t mys = j < J ? submit[j] : 0, myi = j < J ? id[j] : 0;
+  int r = 0;
+  for (int b0 = 0; b0 < J; b0 += 256) {
+    const int i = b0 + threadIdx.x;
+    ss[threadIdx.x] = i < J ? submit[i] : INT64_MAX;
+    si[threadIdx.x] = i < J ? id[i] : INT64_MAX;
+    __syncthreads();
+    const int n = min(256, J - b0);
+    for (int q = 0; q < n; ++q) r += (ss[q] < mys) || (ss[q] == mys && si[q] < myi);
+    __syncthreads();
+  }
+  if (j < J) {
+    rank[j] = r;
+    pi[r] = j;
+  }
+}
+
+// Device-side profile validation: min over c (must be >= 1) and per-job max c
+// (for the §N0 bound L*max(c)*GB < 2^52, checked on the host).
+__global__ void k_profile_stats(Params P, int32_t *job_maxc, int32_t *min_c) {
+  const int j = blockIdx.x;
+  const int64_t off = P.off[j];
+  const int L = P.L[j];
+  int mx = 0, mn = INT32_MAX;
+  for (int tk = 0; tk < P.T * P.K1; ++tk) {
+    const int32_t *row = P.c + (int64_t)tk * P.TL + off;
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+      mx = max(mx, row[l]);
+      mn = min(mn, row[l]);
+    }
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&job_maxc[j], mx);
+    atomicMin(min_c, mn);
+  }
+}
+
+}  // namespace crius

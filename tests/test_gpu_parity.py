@@ -1,0 +1,256 @@
+"""GPU path (libcrius through the C-ABI) vs the CPU oracle, element by element.
+
+Contract (BASELINE.json north_star): Cells, stage splits, plan indices and
+schedule decisions bit-exact; fp64 times (t_ns / 1e9) within 1e-9 relative
+(they are in fact bit-identical: both sides produce the same int64 ns).
+Every input is seeded and synthetic (paper_2403_16125_b200.workload).
+"""
+import numpy as np
+import pytest
+
+from paper_2403_16125_b200 import workload as W
+
+pytestmark = pytest.mark.gpu
+INF = np.iinfo(np.int64).max
+
+
+@pytest.fixture(scope="module")
+def crius():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
+    from paper_2403_16125_b200 import build
+    build.build()
+    import paper_2403_16125_b200 as pkg
+    return pkg
+
+
+def gpu_run(pkg, pr, splits=False, free=None, round_=True):
+    import torch
+    with pkg.Crius(pr) as cr:
+        n, p, u = cr.enumerate()
+        cells = {k: v.cpu().numpy() for k, v in cr.cells().items()}
+        sp = None
+        if splits:
+            sp = torch.full((max(u, 1) * cr.split_stride(),), -7, dtype=torch.int16, device="cuda")
+        res = cr.estimate(splits=sp)
+        t_ns, plan, flags = pkg.decode(res)
+        out = dict(cells=cells, t_ns=t_ns[:n], plan=plan[:n], flags=flags[:n], n=n, p=p, u=u,
+                   stride=cr.split_stride(), launches=cr.launches())
+        if splits:
+            out["splits"] = sp.cpu().numpy().reshape(u, -1)
+        if round_:
+            out["round"] = cr.schedule_round(res, free=free)
+        return out
+
+
+def oracle_run(oracle_mod, pr, free=None, c_range=None):
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    if c_range is None:
+        t_ns, plan = o.estimate(cells)
+    else:
+        t_ns, plan = o.estimate(cells, *c_range)
+    rnd = o.round(cells, t_ns, free_in=free) if c_range is None else None
+    return o, cells, t_ns, plan, rnd
+
+
+def assert_same(g, o_cells, o_t, o_plan, o_round=None):
+    for k in ("job", "type", "G", "S", "nplans"):
+        assert np.array_equal(g["cells"][k], o_cells[k]), k
+    assert np.array_equal(g["t_ns"], o_t)
+    assert np.array_equal(g["plan"], o_plan)
+    assert np.array_equal(g["flags"], (o_plan >= 0).astype(np.int32))
+    # fp64 contract: (double)t_ns / 1e9, relative error <= 1e-9
+    fin = o_t < INF
+    ts_g = g["t_ns"][fin].astype(np.float64) / 1e9
+    ts_o = o_t[fin].astype(np.float64) / 1e9
+    assert np.all(np.abs(ts_g - ts_o) <= 1e-9 * np.abs(ts_o))
+    if o_round is not None:
+        dg, fg, tg = g["round"]
+        do, fo, to = o_round
+        assert np.array_equal(dg, do)
+        assert np.array_equal(fg, fo)
+        assert tg == to and abs(tg - to) <= 1e-9 * abs(to)
+
+
+def check_splits(g, o, pr, sample=None, seed=0):
+    u = g["u"]
+    units = range(u) if sample is None else np.random.default_rng(seed).choice(u, sample, replace=False)
+    ucb = g["cells"]["unit_cell_begin"]
+    for uu in units:
+        row = g["splits"][uu]
+        if ucb[uu + 1] == ucb[uu]:
+            assert np.all(row == -1)
+            continue
+        j, t = divmod(int(uu), pr.n_types)
+        smax = int(g["cells"]["S"][ucb[uu]:ucb[uu + 1]].max())
+        si = 0
+        while (1 << si) <= smax:
+            S = 1 << si
+            at = (S - 1) + si
+            assert np.array_equal(row[at:at + S + 1], o.split(j, t, S)), (uu, S)
+            si += 1
+        assert np.all(row[(1 << si) - 1 + si:] == -1)
+
+
+CONFIGS = [(1, None, True), (1, "sweep", True), (1, None, False), (2, None, True),
+           (3, None, True), (4, None, True)]
+
+
+@pytest.mark.parametrize("cfg,variant,jitter", CONFIGS)
+def test_configs_bit_exact(crius, oracle_mod, cfg, variant, jitter):
+    pr = W.make_config(cfg, variant=variant, jitter=jitter)
+    g = gpu_run(crius, pr, splits=True)
+    o, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr)
+    assert (g["n"], g["p"]) == o.count()
+    assert_same(g, cells, t_ns, plan, rnd)
+    check_splits(g, o, pr, sample=None if g["u"] <= 400 else 300, seed=cfg)
+    assert g["launches"] > 0
+
+
+@pytest.mark.parametrize("seed", [101, 102, 103])
+def test_other_seeds(crius, oracle_mod, seed):
+    for cfg in (2, 3):
+        pr = W.make_config(cfg, seed=seed)
+        g = gpu_run(crius, pr)
+        _, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr)
+        assert_same(g, cells, t_ns, plan, rnd)
+
+
+def test_cfg4_all_pow2(crius, oracle_mod):
+    pr = W.make_config(4, variant="pow2")
+    g = gpu_run(crius, pr, splits=True)
+    _, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr)
+    assert_same(g, cells, t_ns, plan, rnd)
+
+
+def test_cfg5_sampled_units(crius, oracle_mod):
+    """Full-size cfg5 (96 layers, S <= 32, 7 B values): the GPU estimates every
+    Cell; the oracle recomputes the Cells of 200 sampled units one by one."""
+    pr = W.make_config(5)
+    g = gpu_run(crius, pr, splits=True, round_=False)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()  # the oracle's own Cell list, compared with the GPU's
+    for k in ("job", "type", "G", "S", "nplans"):
+        assert np.array_equal(g["cells"][k], cells[k]), k
+    unit = cells["job"].astype(np.int64) * pr.n_types + cells["type"]
+    ucb = np.searchsorted(unit, np.arange(g["u"] + 1), side="left")
+    rng = np.random.default_rng(5)
+    for uu in rng.choice(g["u"], 200, replace=False):
+        c0, c1 = int(ucb[uu]), int(ucb[uu + 1])
+        if c0 == c1:
+            continue
+        t_ns, plan = o.estimate(cells, c0, c1)
+        assert np.array_equal(g["t_ns"][c0:c1], t_ns), uu
+        assert np.array_equal(g["plan"][c0:c1], plan), uu
+    check_splits(g, o, pr, sample=100, seed=55)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_tiny(crius, oracle_mod, seed):
+    pr = W.random_tiny(seed, max_layers=12, n_types=3, n_jobs=6)
+    g = gpu_run(crius, pr, splits=True)
+    o, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr)
+    assert_same(g, cells, t_ns, plan, rnd)
+    check_splits(g, o, pr)
+
+
+def test_edge_uniform_layers_max_ties(crius, oracle_mod):
+    pr = W.make_config(5, jitter=False)
+    pr_small = W.assemble("u", W.CFG4_CLUSTER, ["GPT96"] * 50, pr.ng[:50], pr.gb[:50],
+                          np.random.default_rng(0), jitter=False, gpu_set=1, s_max=32, g_max=64,
+                          b_mode=1, b_values=W.B_SWEEP.copy(), depth=3)
+    g = gpu_run(crius, pr_small, splits=True)
+    o, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr_small)
+    assert_same(g, cells, t_ns, plan, rnd)
+    check_splits(g, o, pr_small)
+
+
+def test_edge_single_layer_and_S_equals_L(crius, oracle_mod):
+    from helpers import problem_from
+    jobs = [dict(c=[5], ng=4, gb=16, w=[10], act=[1], bnd=[3], tpv=[2], tpn=[1]),
+            dict(c=[3, 1, 4, 1, 5, 9, 2, 6], ng=8, gb=64, w=[1] * 8, act=[2] * 8, bnd=[4] * 8,
+                 tpv=[8] * 8, tpn=[2] * 8, submit=1, id=1)]
+    pr = problem_from([dict(cap=16, gpn=4), dict(cap=8, gpn=2)], jobs, k_max=3, g_max=8,
+                      gpu_set=1, s_max=64)
+    g = gpu_run(crius, pr, splits=True)
+    o, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr)
+    assert_same(g, cells, t_ns, plan, rnd)
+    check_splits(g, o, pr)
+    assert (g["cells"]["S"] == 8).any()
+
+
+def test_edge_memory_infeasible_everywhere(crius, oracle_mod):
+    pr = W.make_config(2)
+    pr.mem = np.ones_like(pr.mem)
+    g = gpu_run(crius, pr)
+    _, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr)
+    assert_same(g, cells, t_ns, plan, rnd)
+    assert np.all(g["plan"] == -1) and np.all(g["round"][0] == -2)
+
+
+def test_edge_no_free_gpus(crius, oracle_mod):
+    pr = W.make_config(3)
+    free = np.zeros(pr.n_types, np.int32)
+    g = gpu_run(crius, pr, free=free)
+    _, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr, free=free)
+    assert_same(g, cells, t_ns, plan, rnd)
+    assert np.all(g["round"][0] < 0)
+
+
+@pytest.mark.parametrize("depth", [0, 1, 2, 5])
+def test_round_depths(crius, oracle_mod, depth):
+    pr = W.make_config(3)
+    pr.depth = depth
+    g = gpu_run(crius, pr)
+    _, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr)
+    assert_same(g, cells, t_ns, plan, rnd)
+
+
+def test_rank_invariance_emulated(crius, oracle_mod):
+    """Estimating the contiguous unit ranges of R ranks one after another and
+    compacting the padded chunks gives byte-identical records and decisions."""
+    import torch
+    pkg = crius
+    pr = W.make_config(4)
+    with pkg.Crius(pr) as cr:
+        n, _, u = cr.enumerate()
+        ref = cr.estimate().clone()
+        dec_ref = cr.schedule_round(ref)
+        for world in (2, 4, 8):
+            ub, cb = cr.partition(world)
+            assert ub[0] == 0 and ub[-1] == u and cb[-1] == n and np.all(np.diff(ub) >= 0)
+            chunk = int(max(cb[r + 1] - cb[r] for r in range(world)))
+            gathered = torch.full((world * chunk, 2), -1, dtype=torch.int64, device="cuda")
+            for r in range(world):
+                cr.estimate(ub[r], ub[r + 1], out=gathered[r * chunk:(r + 1) * chunk])
+            full = cr.compact(gathered, chunk, world, cb)
+            assert torch.equal(full[:n], ref[:n])
+            d = cr.schedule_round(full)
+            assert np.array_equal(d[0], dec_ref[0]) and d[2] == dec_ref[2]
+
+
+def test_update_profiles_and_repeat(crius, oracle_mod):
+    pkg = crius
+    a, b = W.make_config(3, seed=3), W.make_config(3, seed=3)
+    b.c = (b.c * 2).astype(np.int32)
+    with pkg.Crius(a) as cr:
+        cr.enumerate()
+        r1 = pkg.decode(cr.estimate())[0]
+        r1b = pkg.decode(cr.estimate())[0]
+        assert np.array_equal(r1, r1b)
+        cr.update(b)
+        cr.enumerate()
+        r2 = pkg.decode(cr.estimate())[0][:cr.n_cells]
+    _, _, t_ns, _, _ = oracle_run(oracle_mod, b)
+    assert np.array_equal(r2, t_ns)
+
+
+def test_loader_rejects_overflow(crius):
+    pkg = crius
+    pr = W.make_config(2)
+    pr.c = np.full_like(pr.c, 2 ** 31 - 1)
+    with pytest.raises(pkg.CriusError) as e:
+        pkg.Crius(pr)
+    assert e.value.code == 2 and "2^52" in str(e.value)
