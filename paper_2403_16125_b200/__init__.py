@@ -116,7 +116,7 @@ class _DevArray:
 
     def __init__(self, ptr, n, typestr, device):
         self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
-                                         "data": (int(ptr or 0), True), "version": 3}
+                                         "data": (int(ptr or 0), False), "version": 3}
         self.device = device
 
 
@@ -272,5 +272,5 @@ def decode(results):
     """[n, 2] int64 device records -> (t_ns int64, plan int32, flags int32) numpy."""
     r = results.cpu().numpy()
     t_ns = r[:, 0].copy()
-    pf = r[:, 1].view(np.int32).reshape(-1, 2)
+    pf = np.ascontiguousarray(r[:, 1]).view(np.int32).reshape(-1, 2)
     return t_ns, pf[:, 0].copy(), pf[:, 1].copy()

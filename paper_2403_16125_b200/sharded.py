@@ -1,0 +1,41 @@
+"""Multi-GPU sharding of the Cell space.
+
+The unit (job, GPU type) is the independent piece of work: its stage DP, every
+Cell (G, S) and every plan depend only on that job's profile rows and that
+type's parameters.  Each rank estimates one contiguous, work-balanced range of
+units (crius_partition_units), so its Cells are one contiguous range; ONE
+all-gather (NCCL over NVLink 5 / NVSwitch through torch.distributed) gives
+every rank every Cell's 16-byte record, the per-rank padding is removed on the
+device (crius_compact_gathered), and every rank runs the same deterministic
+round -- no further exchange is needed.
+
+`ctx` is a `Crius` context (or anything with the same partition / new_results /
+estimate / compact methods).
+"""
+from __future__ import annotations
+
+
+class ShardPlan:
+    """Unit/Cell ranges of every rank and the padded chunk size."""
+
+    def __init__(self, ctx, world):
+        self.world = world
+        self.unit_begin, self.cell_begin = ctx.partition(world)
+        self.chunk = int(max(self.cell_begin[r + 1] - self.cell_begin[r] for r in range(world)))
+        self.n_cells = int(self.cell_begin[world])
+
+
+def estimate_all(ctx, plan: ShardPlan, rank, mine=None, gathered=None, full=None, group=None):
+    """Estimate this rank's range, all-gather all ranks' records, compact.
+    Returns the full [n_cells, 2] record tensor (identical on every rank)."""
+    import torch.distributed as dist
+    w = plan.world
+    if mine is None:
+        mine = ctx.new_results(plan.chunk)
+    ctx.estimate(int(plan.unit_begin[rank]), int(plan.unit_begin[rank + 1]), out=mine)
+    if w == 1:
+        return mine
+    if gathered is None:
+        gathered = ctx.new_results(w * plan.chunk)
+    dist.all_gather_into_tensor(gathered, mine[:plan.chunk], group=group)
+    return ctx.compact(gathered, plan.chunk, w, plan.cell_begin, out=full)

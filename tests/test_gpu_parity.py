@@ -251,6 +251,7 @@ def test_loader_rejects_overflow(crius):
     pkg = crius
     pr = W.make_config(2)
     pr.c = np.full_like(pr.c, 2 ** 31 - 1)
+    pr.gb = np.full_like(pr.gb, 2 ** 20)   # 34 layers * 2^31 ns * 2^20 samples > 2^52
     with pytest.raises(pkg.CriusError) as e:
         pkg.Crius(pr)
     assert e.value.code == 2 and "2^52" in str(e.value)
