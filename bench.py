@@ -370,6 +370,7 @@ def main():
                          "ops_per_launch": ops * frac_units, "dp_probes": probes,
                          "stage_evals": stage_evals,
                          "hbm_gbs": hbm, "hbm_frac": hbm / float(peaks.get("hbm_gbs", 6650.0))},
+            "round_stats": cr.round_stats(),
             "clocks": clocks, "gpu_launches": int(launches)}
     if e2e:
         line["e2e"] = e2e

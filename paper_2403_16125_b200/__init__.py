@@ -67,7 +67,8 @@ class _CellView(C.Structure):
 
 EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_enumerate_cells", "crius_cells",
            "crius_split_stride", "crius_partition_units", "crius_estimate_cells",
-           "crius_compact_gathered", "crius_schedule_round", "crius_kernel_launches",
+           "crius_compact_gathered", "crius_schedule_round", "crius_round_stats",
+           "crius_kernel_launches",
            "crius_last_error", "crius_destroy"]
 
 _lib = None
@@ -93,6 +94,7 @@ def lib():
         L.crius_estimate_cells.argtypes = [vp, i64, i64, vp, vp, vp]
         L.crius_compact_gathered.argtypes = [vp, vp, i64, i32, vp, vp, vp]
         L.crius_schedule_round.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.crius_round_stats.argtypes = [vp, vp, vp]
         L.crius_kernel_launches.argtypes = [vp]
         L.crius_kernel_launches.restype = i64
         L.crius_last_error.restype = C.c_char_p
@@ -246,6 +248,13 @@ class Crius:
         _check(lib().crius_schedule_round(self.ctx, C.c_void_p(results.data_ptr()), fr, _ptr(dec),
                                           _ptr(fa), C.byref(tot), _stream_handle(stream)))
         return dec, fa, tot.value
+
+    def round_stats(self, stream=None):
+        out = np.zeros(8, np.int64)
+        _check(lib().crius_round_stats(self.ctx, _ptr(out), _stream_handle(stream)))
+        keys = ("phaseA_batches", "seq_recomputes", "seq_cycles", "phaseA_cycles", "phaseB_cycles",
+                "admitted", "scale_admits", "phaseB_batches")
+        return dict(zip(keys, (int(x) for x in out)))
 
     def launches(self):
         return lib().crius_kernel_launches(self.ctx)

@@ -84,9 +84,12 @@ struct crius_ctx {
   // round
   int32_t maxopt = 0;
   OptRec *d_opt = nullptr;
+  double *d_score = nullptr;
   int64_t *d_opt_cell = nullptr, *d_ref = nullptr, *d_decision = nullptr;
-  int32_t *d_nopt = nullptr, *d_rng = nullptr, *d_cur = nullptr, *d_adm = nullptr, *d_free = nullptr;
+  int32_t *d_nopt = nullptr, *d_rng = nullptr, *d_cur = nullptr, *d_free = nullptr;
   double *d_total = nullptr;
+  int64_t *d_round_stats = nullptr;
+  AdmView adm_glob{};  // admitted-job records in global memory (only when they exceed shared)
 };
 
 namespace {
@@ -98,7 +101,11 @@ void free_all(crius_ctx *c) {
                   c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight,
                   c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
-                  c->d_rng, c->d_cur, c->d_adm, c->d_free, c->d_total};
+                  c->d_rng, c->d_cur, c->d_free, c->d_total, c->adm_glob.pos,
+                  c->d_round_stats, c->d_score, c->adm_glob.T, c->adm_glob.sc,
+                  c->adm_glob.bi_key, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
+                  c->adm_glob.t, c->adm_glob.nopt, c->adm_glob.bi_opt, c->adm_glob.bi_freed,
+                  c->adm_glob.bi_valid, c->adm_glob.gmin};
   for (void *p : ptrs)
     if (p) cudaFree(p);
 }
@@ -662,15 +669,16 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
   const int J = c->P.J, T = c->P.T;
   if (!c->d_opt) {
     CK(dalloc(&c->d_opt, (size_t)J * c->maxopt));
+    CK(dalloc(&c->d_score, (size_t)J * c->maxopt));
     CK(dalloc(&c->d_opt_cell, (size_t)J * c->maxopt));
     CK(dalloc(&c->d_ref, J));
     CK(dalloc(&c->d_decision, J));
     CK(dalloc(&c->d_nopt, J));
     CK(dalloc(&c->d_rng, J));
     CK(dalloc(&c->d_cur, J));
-    CK(dalloc(&c->d_adm, J));
     CK(dalloc(&c->d_free, 16));
     CK(dalloc(&c->d_total, 1));
+    CK(dalloc(&c->d_round_stats, 8));
   }
   std::vector<int32_t> fr(T);
   for (int t = 0; t < T; ++t) {
@@ -685,26 +693,70 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
   R.depth = c->P.depth;
   R.rank = c->d_rank;
   R.pi = c->d_pi;
-  R.ng_job = c->d_ng;
   R.opt = c->d_opt;
+  R.score = c->d_score;
   R.opt_cell = c->d_opt_cell;
   R.nopt = c->d_nopt;
   R.ref = c->d_ref;
   R.ng = c->d_rng;
   R.cur = c->d_cur;
-  R.adm = c->d_adm;
   R.decision = c->d_decision;
   R.free_io = c->d_free;
   R.total = c->d_total;
+  R.stats = c->d_round_stats;
   k_round_options<<<(J + 127) / 128, 128, 0, st>>>(c->P, c->C.unit_cell_begin, c->C.type, c->C.G,
                                                    (const CellResult *)d_all, R);
   CKL();
-  k_round_greedy<<<1, kRoundThreads, 0, st>>>(R);
+  // each admitted job holds >= 1 GPU: at most min(J, sum of free GPUs) records
+  int64_t max_adm = 0;
+  for (int t = 0; t < T; ++t) max_adm += fr[t];
+  max_adm = std::min<int64_t>(max_adm, J);
+  cudaFuncAttributes fa{};
+  CK(cudaFuncGetAttributes(&fa, k_round_greedy));
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  const size_t budget = (size_t)optin - fa.sharedSizeBytes - 1024;  // dynamic next to static
+  const size_t per_job = (size_t)c->maxopt * (sizeof(OptRec) + 8) + 16;
+  int adm_in_smem = max_adm <= kAdmSmem;
+  size_t adm_bytes = adm_in_smem ? (size_t)kAdmSmem * kAdmBytes : 0;
+  if (adm_in_smem && (budget - adm_bytes) / per_job < 32) {
+    adm_in_smem = 0;
+    adm_bytes = 0;
+  }
+  int win_cap = (int)std::min<size_t>(256, (budget - adm_bytes) / per_job) & ~31;
+  if (win_cap < 32) return fail(CRIUS_EINVAL, "too many options per job for the round's window");
+  const size_t dsm = (size_t)win_cap * per_job + adm_bytes;
+  if (!adm_in_smem && !c->adm_glob.pos) {
+    CK(dalloc(&c->adm_glob.T, J));
+    CK(dalloc(&c->adm_glob.sc, J));
+    CK(dalloc(&c->adm_glob.bi_key, J));
+    CK(dalloc(&c->adm_glob.pos, J));
+    CK(dalloc(&c->adm_glob.cur, J));
+    CK(dalloc(&c->adm_glob.G, J));
+    CK(dalloc(&c->adm_glob.t, J));
+    CK(dalloc(&c->adm_glob.nopt, J));
+    CK(dalloc(&c->adm_glob.bi_opt, J));
+    CK(dalloc(&c->adm_glob.bi_freed, J));
+    CK(dalloc(&c->adm_glob.bi_valid, J));
+    CK(dalloc(&c->adm_glob.gmin, J));
+  }
+  CK(cudaFuncSetAttribute(k_round_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  k_round_greedy<<<1, kRoundThreads, dsm, st>>>(R, adm_in_smem, c->adm_glob, win_cap);
   CKL();
   c->launches += 2;
   CK(cudaMemcpyAsync(decision, c->d_decision, (size_t)J * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(free_after, c->d_free, T * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(total_score, c->d_total, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return CRIUS_OK;
+}
+
+crius_status crius_round_stats(crius_ctx *c, int64_t *out8, void *stream) {
+  if (!c || !out8) return fail(CRIUS_EINVAL, "null argument");
+  if (!c->d_round_stats) return fail(CRIUS_ESTATE, "no round has run");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(out8, c->d_round_stats, 64, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return CRIUS_OK;
 }
