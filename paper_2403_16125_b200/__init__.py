@@ -250,10 +250,12 @@ class Crius:
         return dec, fa, tot.value
 
     def round_stats(self, stream=None):
-        out = np.zeros(8, np.int64)
+        out = np.zeros(16, np.int64)
         _check(lib().crius_round_stats(self.ctx, _ptr(out), _stream_handle(stream)))
         keys = ("phaseA_batches", "seq_recomputes", "seq_cycles", "phaseA_cycles", "phaseB_cycles",
-                "admitted", "scale_admits", "phaseB_batches")
+                "admitted", "scale_admits", "phaseB_batches", "seq_setup_cycles",
+                "seq_same_type_cycles", "seq_other_type_cycles", "seq_reduce_cycles",
+                "stale_caches", "other_type_scans")
         return dict(zip(keys, (int(x) for x in out)))
 
     def launches(self):

@@ -89,6 +89,7 @@ struct crius_ctx {
   int32_t *d_nopt = nullptr, *d_rng = nullptr, *d_cur = nullptr, *d_free = nullptr;
   double *d_total = nullptr;
   int64_t *d_round_stats = nullptr;
+  int32_t *d_list = nullptr;
   AdmView adm_glob{};  // admitted-job records in global memory (only when they exceed shared)
 };
 
@@ -102,10 +103,10 @@ void free_all(crius_ctx *c) {
                   c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
                   c->d_rng, c->d_cur, c->d_free, c->d_total, c->adm_glob.pos,
-                  c->d_round_stats, c->d_score, c->adm_glob.T, c->adm_glob.sc,
-                  c->adm_glob.bi_key, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
-                  c->adm_glob.t, c->adm_glob.nopt, c->adm_glob.bi_opt, c->adm_glob.bi_freed,
-                  c->adm_glob.bi_valid, c->adm_glob.gmin};
+                  c->d_round_stats, c->d_score, c->adm_glob.T, c->adm_glob.bi_T,
+                  c->adm_glob.sc, c->adm_glob.bi_key, c->adm_glob.bi_s, c->adm_glob.pos,
+                  c->adm_glob.cur, c->adm_glob.G, c->adm_glob.t, c->adm_glob.nopt,
+                  c->adm_glob.bi_opt, c->adm_glob.bi_G2, c->adm_glob.gmin, c->d_list};
   for (void *p : ptrs)
     if (p) cudaFree(p);
 }
@@ -667,6 +668,7 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int J = c->P.J, T = c->P.T;
+  if (T > kRT) return fail(CRIUS_EINVAL, "the scheduling round supports at most 8 GPU types");
   if (!c->d_opt) {
     CK(dalloc(&c->d_opt, (size_t)J * c->maxopt));
     CK(dalloc(&c->d_score, (size_t)J * c->maxopt));
@@ -678,7 +680,7 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
     CK(dalloc(&c->d_cur, J));
     CK(dalloc(&c->d_free, 16));
     CK(dalloc(&c->d_total, 1));
-    CK(dalloc(&c->d_round_stats, 8));
+    CK(dalloc(&c->d_round_stats, 16));
   }
   std::vector<int32_t> fr(T);
   for (int t = 0; t < T; ++t) {
@@ -704,6 +706,7 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
   R.free_io = c->d_free;
   R.total = c->d_total;
   R.stats = c->d_round_stats;
+  R.list = c->d_list;
   k_round_options<<<(J + 127) / 128, 128, 0, st>>>(c->P, c->C.unit_cell_begin, c->C.type, c->C.G,
                                                    (const CellResult *)d_all, R);
   CKL();
@@ -728,17 +731,19 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
   const size_t dsm = (size_t)win_cap * per_job + adm_bytes;
   if (!adm_in_smem && !c->adm_glob.pos) {
     CK(dalloc(&c->adm_glob.T, J));
+    CK(dalloc(&c->adm_glob.bi_T, J));
     CK(dalloc(&c->adm_glob.sc, J));
     CK(dalloc(&c->adm_glob.bi_key, J));
+    CK(dalloc(&c->adm_glob.bi_s, J));
     CK(dalloc(&c->adm_glob.pos, J));
     CK(dalloc(&c->adm_glob.cur, J));
     CK(dalloc(&c->adm_glob.G, J));
     CK(dalloc(&c->adm_glob.t, J));
     CK(dalloc(&c->adm_glob.nopt, J));
     CK(dalloc(&c->adm_glob.bi_opt, J));
-    CK(dalloc(&c->adm_glob.bi_freed, J));
-    CK(dalloc(&c->adm_glob.bi_valid, J));
+    CK(dalloc(&c->adm_glob.bi_G2, J));
     CK(dalloc(&c->adm_glob.gmin, J));
+    CK(dalloc(&c->d_list, J));
   }
   CK(cudaFuncSetAttribute(k_round_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   k_round_greedy<<<1, kRoundThreads, dsm, st>>>(R, adm_in_smem, c->adm_glob, win_cap);
@@ -751,12 +756,13 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
   return CRIUS_OK;
 }
 
-crius_status crius_round_stats(crius_ctx *c, int64_t *out8, void *stream) {
-  if (!c || !out8) return fail(CRIUS_EINVAL, "null argument");
+crius_status crius_round_stats(crius_ctx *c, int64_t *out16, void *stream) {
+  int64_t *out8 = out16;
+  if (!c || !out16) return fail(CRIUS_EINVAL, "null argument");
   if (!c->d_round_stats) return fail(CRIUS_ESTATE, "no round has run");
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemcpyAsync(out8, c->d_round_stats, 64, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out8, c->d_round_stats, 128, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return CRIUS_OK;
 }

@@ -47,7 +47,8 @@ struct RoundBuf {
   int64_t *decision;     // [J] by job
   int32_t *free_io;      // [T]
   double *total;
-  int64_t *stats;        // [8] counters (see crius_round_stats)
+  int64_t *stats;        // [16] counters (see crius_round_stats)
+  int32_t *list;         // [J] scratch list (used when admitted records live in global memory)
 };
 
 __device__ __forceinline__ double score_of(int64_t ref, int64_t T) {
@@ -106,17 +107,20 @@ __device__ __forceinline__ bool kappa_less(const OptRec &a, const OptRec &b) {
 }
 
 constexpr int kRoundThreads = 1024;
+constexpr int kRT = 8;  // GPU types supported by the round kernel (shared-memory tables)
 constexpr int kRoundWarps = kRoundThreads / 32;
 constexpr int kAdmSmem = 2048;  // admitted-job records kept in shared memory up to this many
-constexpr int kAdmBytes = 60;   // bytes per admitted-job record
+constexpr int kAdmBytes = 76;   // bytes per admitted-job record (incl. scratch list)
 
 // Admitted jobs, in priority order (SoA; shared memory when they fit, else global).
-// bi_* caches the job's best same-type victim move (case (i)), which depends
-// only on its current option; bi_valid = 0 after every change of that option.
+// bi_* caches the job's best same-type victim move (case (i) of ScaleResource),
+// which depends only on its current option: bi_opt = -2 marks a stale cache
+// (set whenever the option changes), -1 = no such move.  gmin = the job's
+// smallest option G (an other-type move (ii) needs G_o' <= free'[t_o']).
 struct AdmView {
-  int64_t *T;
-  double *sc, *bi_key;
-  int32_t *pos, *cur, *G, *t, *nopt, *bi_opt, *bi_freed, *bi_valid, *gmin;
+  int64_t *T, *bi_T;
+  double *sc, *bi_key, *bi_s;
+  int32_t *pos, *cur, *G, *t, *nopt, *bi_opt, *bi_G2, *gmin;
 };
 
 // Window of upcoming jobs (priority positions [w0, w0 + wn)) staged in shared memory.
@@ -129,35 +133,69 @@ struct JobWin {
 };
 
 struct RoundShared {
-  int32_t fr[kMaxTypes];
-  int32_t n_adm, seq_valid, advance, any_change, win0;
+  int32_t fr[kRT];
+  int32_t n_adm, seq_valid, advance, any_change, n_dirty, n_list;
+  long long prof[8];  // cycles: [0] setup+dirty, [1] (i) pass, [2] (ii) pass, [3] reduce+apply; [4] dirty jobs, [5] listed jobs
   // victim-move sequences, one per GPU type, cut at <= d moves
-  int32_t len[kMaxTypes], active[kMaxTypes];
-  int32_t mv_a[kMaxTypes][kMaxDepth], mv_opt[kMaxTypes][kMaxDepth];
-  int32_t mv_G[kMaxTypes][kMaxDepth], mv_t[kMaxTypes][kMaxDepth];   // the victim's new option
-  int64_t mv_T[kMaxTypes][kMaxDepth];
-  double mv_sc[kMaxTypes][kMaxDepth];
-  int32_t fmax_other[kMaxTypes];  // max_{t2 != t} free'[t2] of the current move
-  double cum[kMaxTypes][kMaxDepth + 1];                 // ((0 + loss_1) + loss_2) + ...
-  int32_t frs[kMaxTypes][kMaxDepth + 1][kMaxTypes];      // free' after m moves
+  int32_t len[kRT], active[kRT];
+  int32_t mv_a[kRT][kMaxDepth], mv_opt[kRT][kMaxDepth];
+  int32_t mv_G[kRT][kMaxDepth], mv_t[kRT][kMaxDepth];  // the victim's new option
+  int64_t mv_T[kRT][kMaxDepth];
+  double mv_sc[kRT][kMaxDepth];
+  double cum[kRT][kMaxDepth + 1];                 // ((0 + loss_1) + loss_2) + ...
+  int32_t frs[kRT][kMaxDepth + 1][kRT];      // free' after m moves
+  int32_t fmax_other[kRT];                         // max_{t2 != t} free'[t2]
   // per-warp outcome of one speculative batch
   int32_t res_kind[kRoundWarps], res_opt[kRoundWarps], res_m[kRoundWarps], need[kRoundWarps];
   int32_t res_G[kRoundWarps], res_t[kRoundWarps];
   int64_t res_T[kRoundWarps];
   double res_sc[kRoundWarps];
-  // per-(type, warp) argmin scratch
-  double r_key[kMaxTypes][kRoundWarps];
-  int32_t r_a[kMaxTypes][kRoundWarps], r_i[kMaxTypes][kRoundWarps];
-  int32_t r_freed[kMaxTypes][kRoundWarps], r_other[kMaxTypes][kRoundWarps];
+  // per-(type, warp) best move of the current step, with the move's option data
+  double r_key[kRT][kRoundWarps], r_s2[kRT][kRoundWarps];
+  int64_t r_T2[kRT][kRoundWarps];
+  int32_t r_a[kRT][kRoundWarps], r_i[kRT][kRoundWarps];
+  int32_t r_freed[kRT][kRoundWarps], r_other[kRT][kRoundWarps];
+  int32_t r_G2[kRT][kRoundWarps], r_t2[kRT][kRoundWarps];
 };
 
+// ---- warp argmin by lexicographic 3-word keys, one redux.sync per word ------
+// Order-preserving u64 image of a double (no NaN; -0.0 normalised to +0.0).
+__device__ __forceinline__ uint64_t ord_double(double x) {
+  if (x == 0.0) x = 0.0;
+  const long long b = __double_as_longlong(x);
+  return b < 0 ? ~(uint64_t)b : ((uint64_t)b | 0x8000000000000000ull);
+}
+
+// Lane holding the minimum (k, tie) over the lanes with `valid`, or -1.
+__device__ __forceinline__ int warp_lex_argmin(bool valid, uint64_t k, uint32_t tie) {
+  if (!__ballot_sync(0xffffffffu, valid)) return -1;
+  // every lane executes every collective (no short-circuit around redux.sync)
+  const uint32_t hi = valid ? (uint32_t)(k >> 32) : 0xffffffffu;
+  const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
+  valid = valid && hi == mhi;
+  const uint32_t lo = valid ? (uint32_t)k : 0xffffffffu;
+  const uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
+  valid = valid && lo == mlo;
+  const uint32_t tt = valid ? tie : 0xffffffffu;
+  const uint32_t mtt = __reduce_min_sync(0xffffffffu, tt);
+  valid = valid && tt == mtt;
+  return __ffs(__ballot_sync(0xffffffffu, valid)) - 1;
+}
+
+// kappa(o) = (T, G, t): G is a power of two, so (log2 G, t) orders like (G, t).
+__device__ __forceinline__ uint32_t kappa_tie(const OptRec &x) {
+  return ((uint32_t)ilog2_pow2((uint32_t)x.G) << 8) | (uint32_t)x.t;
+}
+
+// A victim move: key = loss / freed, ordered by (key, admitted index a, option i).
 struct Cand {
   int have;
   double key;
-  int a, i, freed, other;
+  int a, i, freed, other, G2, t2;
+  int64_t T2;
+  double s2;
 };
 
-// (key, admitted index = priority order, option index = (t, G) order) ascending
 __device__ __forceinline__ bool cand_less(const Cand &x, const Cand &y) {
   if (!x.have) return false;
   if (!y.have) return true;
@@ -166,197 +204,209 @@ __device__ __forceinline__ bool cand_less(const Cand &x, const Cand &y) {
   return x.i < y.i;
 }
 
-__device__ __forceinline__ Cand warp_min_cand(Cand c) {
-  for (int d = 16; d > 0; d >>= 1) {
-    Cand o;
-    o.have = __shfl_xor_sync(0xffffffffu, c.have, d);
-    o.key = __shfl_xor_sync(0xffffffffu, c.key, d);
-    o.a = __shfl_xor_sync(0xffffffffu, c.a, d);
-    o.i = __shfl_xor_sync(0xffffffffu, c.i, d);
-    o.freed = __shfl_xor_sync(0xffffffffu, c.freed, d);
-    o.other = __shfl_xor_sync(0xffffffffu, c.other, d);
-    if (cand_less(o, c)) c = o;
-  }
-  return c;
+// Warp-wide argmin of Cands (one per lane) -> winning lane or -1.
+__device__ __forceinline__ int warp_cand_argmin(const Cand &c) {
+  return warp_lex_argmin(c.have, ord_double(c.key), ((uint32_t)c.a << 8) | (uint32_t)c.i);
 }
 
-// Best victim move of admitted job a for the sequence of its own type t under
-// free' = f2 (§N6 ScaleResource candidates; key = loss / freed, loss =
-// score(cur) - score(o')).  Exact shortcuts:
-//  (i)  same type, smaller G: independent of free' -> cached per current option;
-//  (ii) other type with G_o' <= free'[t_o']: impossible when the job's smallest
-//       option G exceeds every other type's free' (fmax); otherwise freed =
-//       G_cur, a power of two, so key = loss * 2^-log2(G_cur) exactly (no
-//       rounding): min key <=> min rounded loss (ties -> lowest option index),
-//       one division for the winner.
-// Option records are fetched 4 at a time with all loads in flight.
-__device__ __forceinline__ Cand eval_victim(const RoundBuf &R, const AdmView &A, int a, int t,
-                                            const int32_t *f2, int fmax) {
-  const int v = A.pos[a], cv = A.cur[a], Gc = A.G[a], nv = A.nopt[a];
+// Per-(type, warp) best-move slot: written only by the winning lane of its warp.
+__device__ __forceinline__ bool slot_take(RoundShared &sh, int t, int w, const Cand &c) {
+  const int sa = sh.r_a[t][w];
+  if (!c.have) return false;
+  if (sa >= 0) {
+    const double sk = sh.r_key[t][w];
+    if (!(c.key < sk || (c.key == sk && (c.a < sa || (c.a == sa && c.i < sh.r_i[t][w])))))
+      return false;
+  }
+  sh.r_key[t][w] = c.key;
+  sh.r_a[t][w] = c.a;
+  sh.r_i[t][w] = c.i;
+  sh.r_freed[t][w] = c.freed;
+  sh.r_other[t][w] = c.other;
+  sh.r_G2[t][w] = c.G2;
+  sh.r_t2[t][w] = c.t2;
+  sh.r_T2[t][w] = c.T2;
+  sh.r_s2[t][w] = c.s2;
+  return true;
+}
+
+// Warp: refresh the same-type move cache (case (i)) and gmin of admitted job a.
+// Lanes cover the job's options (coalesced 16-byte records, one round trip).
+__device__ __forceinline__ void refresh_victim_cache(const RoundBuf &R, const AdmView &A, int a) {
+  const int lane = threadIdx.x & 31;
+  const int v = A.pos[a], cv = A.cur[a], Gc = A.G[a], t = A.t[a], nv = A.nopt[a];
   const double sc = A.sc[a];
-  const longlong2 *ov = reinterpret_cast<const longlong2 *>(R.opt + (int64_t)v * R.maxopt);
-  const double *so = R.score + (int64_t)v * R.maxopt;
-  Cand best{0, 0.0, a, 0, 0, 0};
-  if (!A.bi_valid[a]) {
-    int bi = -1, bf = 0, gmin = INT32_MAX;
-    double bk = 0.0;
-    for (int i0 = 0; i0 < nv; i0 += 4) {
-      longlong2 buf[4];
-      double sb[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (i0 + u < nv) {
-          buf[u] = ov[i0 + u];
-          sb[u] = so[i0 + u];
-        }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i2 = i0 + u;
-        if (i2 >= nv) continue;
-        const int G2 = (int)(buf[u].y & 0xffffffff), t2 = (int)(buf[u].y >> 32);
-        gmin = min(gmin, G2);
-        if (i2 == cv || t2 != t || G2 >= Gc) continue;
-        const double key = __ddiv_rn(sc - sb[u], (double)(Gc - G2));
-        if (bi < 0 || key < bk) {
-          bi = i2;
-          bk = key;
-          bf = Gc - G2;
-        }
-      }
-    }
-    A.bi_opt[a] = bi;
-    A.bi_key[a] = bk;
-    A.bi_freed[a] = bf;
-    A.gmin[a] = gmin;
-    A.bi_valid[a] = 1;
-  }
-  if (A.bi_opt[a] >= 0) {
-    best.have = 1;
-    best.key = A.bi_key[a];
-    best.i = A.bi_opt[a];
-    best.freed = A.bi_freed[a];
-    best.other = 0;
-  }
-  if (A.gmin[a] > fmax) return best;
-  int ii = -1;
-  double lmin = 0.0;
-  for (int i0 = 0; i0 < nv; i0 += 4) {
-    longlong2 buf[4];
-    double sb[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (i0 + u < nv) {
-        buf[u] = ov[i0 + u];
-        sb[u] = so[i0 + u];
-      }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i2 = i0 + u;
-      if (i2 >= nv) continue;
-      const int G2 = (int)(buf[u].y & 0xffffffff), t2 = (int)(buf[u].y >> 32);
-      if (t2 == t || G2 > f2[t2]) continue;
-      const double loss = sc - sb[u];
-      if (ii < 0 || loss < lmin) {
-        ii = i2;
-        lmin = loss;
-      }
-    }
-  }
-  if (ii >= 0) {
-    Cand c{1, __ddiv_rn(lmin, (double)Gc), a, ii, Gc, 1};
+  Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0};
+  int gmin = INT32_MAX;
+  for (int i2 = lane; i2 < nv; i2 += 32) {
+    const OptRec o2 = R.opt[(int64_t)v * R.maxopt + i2];
+    gmin = min(gmin, o2.G);
+    if (i2 == cv || o2.t != t || o2.G >= Gc) continue;
+    const double s2 = R.score[(int64_t)v * R.maxopt + i2];
+    Cand c{1, __ddiv_rn(sc - s2, (double)(Gc - o2.G)), a, i2, Gc - o2.G, 0, o2.G, o2.t, o2.T, s2};
     if (cand_less(c, best)) best = c;
   }
-  return best;
+  gmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)gmin);
+  const int src = warp_cand_argmin(best);
+  if (src < 0) {
+    if (lane == 0) A.bi_opt[a] = -1;
+  } else if (lane == src) {
+    A.bi_opt[a] = best.i;
+    A.bi_key[a] = best.key;
+    A.bi_G2[a] = best.G2;
+    A.bi_T[a] = best.T2;
+    A.bi_s[a] = best.s2;
+  }
+  if (lane == 0) A.gmin[a] = gmin;
+}
+
+// Warp: best other-type move (case (ii)) of admitted job a under free' = f2;
+// the winning lane offers it to the (type, warp) slot.  freed = G_cur is a
+// power of two, so key = loss * 2^-log2(G_cur) exactly: the minimum key is the
+// minimum rounded loss (ties -> lowest option index), one division.
+__device__ __forceinline__ void other_type_move(RoundShared &sh, const RoundBuf &R,
+                                                const AdmView &A, int a, const int32_t *f2) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int v = A.pos[a], Gc = A.G[a], t = A.t[a], nv = A.nopt[a];
+  const double sc = A.sc[a];
+  Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0};
+  for (int i2 = lane; i2 < nv; i2 += 32) {
+    const OptRec o2 = R.opt[(int64_t)v * R.maxopt + i2];
+    if (o2.t == t || o2.G > f2[o2.t]) continue;
+    const double s2 = R.score[(int64_t)v * R.maxopt + i2];
+    Cand c{1, sc - s2, a, i2, Gc, 1, o2.G, o2.t, o2.T, s2};  // key holds the loss here
+    if (cand_less(c, best)) best = c;
+  }
+  const int src = warp_cand_argmin(best);
+  if (lane == src) {
+    best.key = __ddiv_rn(best.key, (double)Gc);
+    slot_take(sh, t, wid, best);
+  }
+  __syncwarp();
 }
 
 // All threads: the greedy victim sequence of every GPU type t from the current
 // state (the §N6 ScaleResource move loop run for d moves without the G_o stop;
 // an option on type t uses the shortest prefix that frees G_o).  Each admitted
-// job is a candidate only for the sequence of its own current type, so one
-// pass over the admitted jobs serves every type's next move.
-__device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmView &A) {
+// job is a candidate only for the sequence of its own current type.  Per move,
+// in one pass: cached same-type moves of every job (shared memory only), and
+// other-type moves of the few jobs whose smallest option could fit free'[t2].
+__device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmView &A,
+                                 int32_t *list) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int TT = R.T, n_adm = sh.n_adm;
   if (tid < TT) {
     sh.len[tid] = 0;
     sh.active[tid] = 1;
     sh.cum[tid][0] = 0.0;
+    int fm = -1;
+    for (int q = 0; q < TT; ++q)
+      if (q != tid) fm = max(fm, sh.fr[q]);
+    sh.fmax_other[tid] = fm;
   }
   if (tid < TT * TT) sh.frs[tid / TT][0][tid % TT] = sh.fr[tid % TT];
+  if (lane < TT) sh.r_a[lane][wid] = -1;
+  if (tid == 0) sh.n_dirty = 0;
+  long long t0 = clock64();
   __syncthreads();
+  // stale same-type caches -> list -> one warp per job
+  for (int a = tid; a < n_adm; a += kRoundThreads)
+    if (A.bi_opt[a] == -2) list[atomicAdd(&sh.n_dirty, 1)] = a;
+  __syncthreads();
+  for (int k = wid; k < sh.n_dirty; k += kRoundWarps) refresh_victim_cache(R, A, list[k]);
+  __syncthreads();
+  if (tid == 0) {
+    const long long t1 = clock64();
+    sh.prof[0] += t1 - t0;
+    sh.prof[4] += sh.n_dirty;
+    t0 = t1;
+  }
+
   for (int m = 0; m < R.depth; ++m) {
-    if (tid < TT) {
-      int fm = -1;
-      for (int q = 0; q < TT; ++q)
-        if (q != tid) fm = max(fm, sh.frs[tid][m][q]);
-      sh.fmax_other[tid] = fm;
-    }
+    if (tid == 0) sh.n_list = 0;
     __syncthreads();
-    Cand run{0, 0.0, 0, 0, 0, 0};  // lane t < TT: this warp's best for type t
     for (int a0 = 0; a0 < n_adm; a0 += kRoundThreads) {
       const int a = a0 + tid;
-      Cand mine{0, 0.0, 0, 0, 0, 0};
+      Cand mine{0, 0.0, 0, 0, 0, 0, 0, 0, 0, 0.0};
       int myt = -1;
       if (a < n_adm) {
         myt = A.t[a];
         bool moved = !sh.active[myt];
         for (int q = 0; q < m; ++q) moved |= sh.mv_a[myt][q] == a;
-        if (!moved) mine = eval_victim(R, A, a, myt, sh.frs[myt][m], sh.fmax_other[myt]);
-      }
-      for (int t = 0; t < TT; ++t) {
-        if (!__ballot_sync(0xffffffffu, myt == t && mine.have)) continue;
-        Cand c = mine;
-        if (myt != t) c.have = 0;
-        c = warp_min_cand(c);
-        if (lane == t && cand_less(c, run)) run = c;
-      }
-    }
-    if (lane < TT) {
-      sh.r_key[lane][wid] = run.key;
-      sh.r_a[lane][wid] = run.have ? run.a : -1;
-      sh.r_i[lane][wid] = run.i;
-      sh.r_freed[lane][wid] = run.freed;
-      sh.r_other[lane][wid] = run.other;
-    }
-    __syncthreads();
-    if (wid < TT && sh.active[wid]) {  // warp t reduces type t and applies its move
-      const int t = wid;
-      Cand c;
-      c.have = sh.r_a[t][lane] >= 0;
-      c.key = sh.r_key[t][lane];
-      c.a = sh.r_a[t][lane];
-      c.i = sh.r_i[t][lane];
-      c.freed = sh.r_freed[t][lane];
-      c.other = sh.r_other[t][lane];
-      c = warp_min_cand(c);
-      if (lane == 0) {
-        if (!c.have) {
-          sh.active[t] = 0;
-        } else {
-          const int v = A.pos[c.a];
-          const OptRec o2 = R.opt[(int64_t)v * R.maxopt + c.i];
-          const double loss = A.sc[c.a] - R.score[(int64_t)v * R.maxopt + c.i];
-          sh.mv_a[t][m] = c.a;
-          sh.mv_opt[t][m] = c.i;
-          sh.mv_G[t][m] = o2.G;
-          sh.mv_t[t][m] = o2.t;
-          sh.mv_T[t][m] = o2.T;
-          sh.mv_sc[t][m] = R.score[(int64_t)v * R.maxopt + c.i];
-          sh.cum[t][m + 1] = __dadd_rn(sh.cum[t][m], loss);
-          for (int q = 0; q < TT; ++q) sh.frs[t][m + 1][q] = sh.frs[t][m][q];
-          sh.frs[t][m + 1][t] += c.freed;
-          if (c.other) sh.frs[t][m + 1][o2.t] -= o2.G;
-          sh.len[t] = m + 1;
+        if (!moved) {
+          const int bo = A.bi_opt[a];
+          if (bo >= 0)
+            mine = Cand{1, A.bi_key[a], a, bo, A.G[a] - A.bi_G2[a], 0, A.bi_G2[a], myt, A.bi_T[a],
+                        A.bi_s[a]};
+          if (A.gmin[a] <= sh.fmax_other[myt]) list[atomicAdd(&sh.n_list, 1)] = a;
         }
       }
+      // (i) cached same-type moves: per type, the warp's winner offers itself
+      for (int t = 0; t < TT; ++t) {
+        const bool v = myt == t && mine.have;
+        const int src = warp_lex_argmin(v, ord_double(mine.key), ((uint32_t)a << 8) | (uint32_t)mine.i);
+        if (lane == src) slot_take(sh, t, wid, mine);
+        __syncwarp();
+      }
     }
     __syncthreads();
+    // (ii) other-type moves of the listed jobs, one warp per job (balanced)
+    for (int k = wid; k < sh.n_list; k += kRoundWarps) {
+      const int aa = list[k];
+      other_type_move(sh, R, A, aa, sh.frs[A.t[aa]][m]);
+    }
+    if (tid == 0) sh.prof[5] += sh.n_list;
+    __syncthreads();
+    if (tid == 0) {
+      const long long t1 = clock64();
+      sh.prof[1] += t1 - t0;
+      t0 = t1;
+    }
+    if (wid < TT && sh.active[wid]) {  // warp t reduces type t, applies its move, preps m+1
+      const int t = wid;
+      const int ra = sh.r_a[t][lane];
+      const int src = warp_lex_argmin(ra >= 0, ord_double(sh.r_key[t][lane]),
+                                      ((uint32_t)ra << 8) | (uint32_t)sh.r_i[t][lane]);
+      if (src < 0) {
+        if (lane == 0) sh.active[t] = 0;
+      } else {
+        if (lane == 0) {
+          const int ca = sh.r_a[t][src];
+          sh.mv_a[t][m] = ca;
+          sh.mv_opt[t][m] = sh.r_i[t][src];
+          sh.mv_G[t][m] = sh.r_G2[t][src];
+          sh.mv_t[t][m] = sh.r_t2[t][src];
+          sh.mv_T[t][m] = sh.r_T2[t][src];
+          sh.mv_sc[t][m] = sh.r_s2[t][src];
+          const double loss = A.sc[ca] - sh.r_s2[t][src];
+          sh.cum[t][m + 1] = __dadd_rn(sh.cum[t][m], loss);
+          int fm = -1;
+          for (int q = 0; q < TT; ++q) {
+            int f = sh.frs[t][m][q];
+            if (q == t) f += sh.r_freed[t][src];
+            if (q == sh.r_t2[t][src] && sh.r_other[t][src]) f -= sh.r_G2[t][src];
+            sh.frs[t][m + 1][q] = f;
+            if (q != t) fm = max(fm, f);
+          }
+          sh.fmax_other[t] = fm;
+          sh.len[t] = m + 1;
+        }
+        __syncwarp();
+        sh.r_a[t][lane] = -1;  // reset this type's slots for move m + 1
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const long long t1 = clock64();
+      sh.prof[3] += t1 - t0;
+      t0 = t1;
+    }
   }
   if (tid == 0) sh.seq_valid = 1;
   __syncthreads();
 }
 
-// Warp-wide argmin of kappa over `nopt` option records passing `pred`.
+// Warp-wide argmin of kappa over `nopt` option records passing `pred` -> index or -1.
 template <typename Pred>
 __device__ __forceinline__ int warp_best_option(const OptRec *o, int nopt, Pred pred) {
   const int lane = threadIdx.x & 31;
@@ -369,18 +419,8 @@ __device__ __forceinline__ int warp_best_option(const OptRec *o, int nopt, Pred 
       bo = x;
     }
   }
-  for (int d = 16; d > 0; d >>= 1) {
-    const int ob = __shfl_xor_sync(0xffffffffu, best, d);
-    const int64_t oT = __shfl_xor_sync(0xffffffffu, bo.T, d);
-    const int oG = __shfl_xor_sync(0xffffffffu, bo.G, d);
-    const int ot = __shfl_xor_sync(0xffffffffu, bo.t, d);
-    const OptRec ox{oT, oG, ot};
-    if (ob >= 0 && (best < 0 || kappa_less(ox, bo))) {
-      best = ob;
-      bo = ox;
-    }
-  }
-  return best;
+  const int src = warp_lex_argmin(best >= 0, (uint64_t)bo.T, kappa_tie(bo));
+  return src < 0 ? -1 : __shfl_sync(0xffffffffu, best, src);
 }
 
 // (Re)point admitted record a at option `opt` (G, t, T, score) of job `pos`.
@@ -392,7 +432,7 @@ __device__ __forceinline__ void adm_set(const AdmView &A, const RoundBuf &R, int
   A.t[a] = t;
   A.T[a] = T;
   A.sc[a] = sc;
-  A.bi_valid[a] = 0;
+  A.bi_opt[a] = -2;
   R.cur[pos] = opt;
 }
 
@@ -444,23 +484,26 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
   AdmView A = Aglob;
   if (adm_in_smem) {
     A.T = (int64_t *)p;
-    A.sc = (double *)(A.T + kAdmSmem);
+    A.bi_T = A.T + kAdmSmem;
+    A.sc = (double *)(A.bi_T + kAdmSmem);
     A.bi_key = A.sc + kAdmSmem;
-    A.pos = (int32_t *)(A.bi_key + kAdmSmem);
+    A.bi_s = A.bi_key + kAdmSmem;
+    A.pos = (int32_t *)(A.bi_s + kAdmSmem);
     A.cur = A.pos + kAdmSmem;
     A.G = A.cur + kAdmSmem;
     A.t = A.G + kAdmSmem;
     A.nopt = A.t + kAdmSmem;
     A.bi_opt = A.nopt + kAdmSmem;
-    A.bi_freed = A.bi_opt + kAdmSmem;
-    A.bi_valid = A.bi_freed + kAdmSmem;
-    A.gmin = A.bi_valid + kAdmSmem;
+    A.bi_G2 = A.bi_opt + kAdmSmem;
+    A.gmin = A.bi_G2 + kAdmSmem;
   }
+  int32_t *list = adm_in_smem ? (int32_t *)(A.gmin + kAdmSmem) : R.list;
   if (tid < TT) sh.fr[tid] = R.free_io[tid];
   if (tid == 0) {
     sh.n_adm = 0;
     sh.seq_valid = 0;
   }
+  if (tid < 8) sh.prof[tid] = 0;
   __syncthreads();
   long long c_start = clock64(), c_seq = 0, n_batches = 0, n_seq = 0, n_scale = 0, n_bb = 0;
   load_window(W, R, 0);
@@ -496,7 +539,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
     if (nmask) {
       if (!sh.seq_valid) {
         const long long c0 = clock64();
-        compute_all_seqs(sh, R, A);
+        compute_all_seqs(sh, R, A, list);
         c_seq += clock64() - c0;
         ++n_seq;
       }
@@ -523,19 +566,9 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
             bm = m;
           }
         }
-        for (int d = 16; d > 0; d >>= 1) {
-          const int ob = __shfl_xor_sync(0xffffffffu, best, d);
-          const int om = __shfl_xor_sync(0xffffffffu, bm, d);
-          const int64_t oT = __shfl_xor_sync(0xffffffffu, bo.T, d);
-          const int oG = __shfl_xor_sync(0xffffffffu, bo.G, d);
-          const int ot = __shfl_xor_sync(0xffffffffu, bo.t, d);
-          const OptRec ox{oT, oG, ot};
-          if (ob >= 0 && (best < 0 || kappa_less(ox, bo))) {
-            best = ob;
-            bo = ox;
-            bm = om;
-          }
-        }
+        const int src = warp_lex_argmin(best >= 0, (uint64_t)bo.T, kappa_tie(bo));
+        best = src < 0 ? -1 : __shfl_sync(0xffffffffu, best, src);
+        bm = src < 0 ? 0 : __shfl_sync(0xffffffffu, bm, src);
         if (lane == 0 && best >= 0) {
           sh.res_kind[wid] = 2;
           sh.res_opt[wid] = best;
@@ -639,6 +672,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       R.stats[5] = n_adm;
       R.stats[6] = n_scale;
       R.stats[7] = n_bb;
+      for (int q = 0; q < 6; ++q) R.stats[8 + q] = sh.prof[q];
     }
   }
   __syncthreads();
