@@ -149,7 +149,8 @@ def committed_traffic(name):
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return d.get(name)
+        e = d.get(name)
+        return None if e is None else e["bytes_per_launch"]
     return None
 
 
@@ -240,6 +241,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2403_16125_b200 as pkg
+    from paper_2403_16125_b200 import sharded
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -250,11 +252,11 @@ def main():
     pr = W.make_config(a.config, variant=a.variant, scale=a.scale)
     cr = pkg.Crius(pr, device=local)
     n_cells, n_plans, n_units = cr.enumerate()
-    ub, cb = cr.partition(world)
-    chunk = int(max(cb[r + 1] - cb[r] for r in range(world)))
-    mine = cr.new_results(chunk)
-    gathered = cr.new_results(world * chunk) if world > 1 else None
-    full = cr.new_results(n_cells)
+    plan = sharded.ShardPlan(cr, world)
+    ub = plan.unit_begin
+    mine = cr.new_results(plan.chunk)
+    gathered = cr.new_results(world * plan.chunk) if world > 1 else None
+    full = cr.new_results(n_cells) if world > 1 else None
     cells_h = {k: v.cpu().numpy() for k, v in cr.cells().items()}
     flush = not a.no_flush
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
@@ -266,13 +268,13 @@ def main():
         e0.record(stream)
         cr.enumerate()
         if world > 1:
-            cr.partition(world)
+            sharded.ShardPlan(cr, world)  # partition is part of the step (a tiny kernel + D2H)
         e1.record(stream)
-        cr.estimate(ub[rank], ub[rank + 1], out=mine)
+        cr.estimate(int(ub[rank]), int(ub[rank + 1]), out=mine)
         e2.record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, mine)
-            res = cr.compact(gathered, chunk, world, cb, out=full)
+            dist.all_gather_into_tensor(gathered, mine[:plan.chunk])
+            res = cr.compact(gathered, plan.chunk, world, plan.cell_begin, out=full)
         else:
             res = mine
         e3.record(stream)
