@@ -177,12 +177,15 @@ crius_status crius_schedule_round(crius_ctx *ctx, const crius_cell_result *d_all
                                   const int32_t *free_gpus, int64_t *decision,
                                   int32_t *free_after, double *total_score, void *stream);
 
-/* Counters of the last round (HOST out16[16]): [0] speculative Phase A batches,
+/* Counters of the last round (HOST out16[21]): [0] speculative Phase A batches,
  * [1] victim-sequence recomputations, [2] SM cycles in them, [3] SM cycles of
  * Phase A, [4] SM cycles of Phase B, [5] admitted jobs, [6] admissions through
  * ScaleResource, [7] Phase B batches, [8..13] cycle/size breakdown of the
  * sequence passes (setup, same-type pass, other-type pass, reduce+apply, stale
- * caches refreshed, other-type jobs scanned).  Synchronises `stream`. */
+ * caches refreshed, other-type jobs scanned), [14] per-type sequence
+ * invalidations, [15..18] cycles of the Phase A
+ * batches (window staging, evaluation, ScaleResource incl. sequences, commit).
+ * Synchronises `stream`. */
 crius_status crius_round_stats(crius_ctx *ctx, int64_t *out16, void *stream);
 
 /* Number of kernels this context has launched so far (for launch accounting). */

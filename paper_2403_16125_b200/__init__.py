@@ -250,12 +250,13 @@ class Crius:
         return dec, fa, tot.value
 
     def round_stats(self, stream=None):
-        out = np.zeros(16, np.int64)
+        out = np.zeros(21, np.int64)
         _check(lib().crius_round_stats(self.ctx, _ptr(out), _stream_handle(stream)))
         keys = ("phaseA_batches", "seq_recomputes", "seq_cycles", "phaseA_cycles", "phaseB_cycles",
                 "admitted", "scale_admits", "phaseB_batches", "seq_setup_cycles",
                 "seq_same_type_cycles", "seq_other_type_cycles", "seq_reduce_cycles",
-                "stale_caches", "other_type_scans")
+                "stale_caches", "other_type_scans", "seq_invalidations", "batch_window_cycles",
+                "batch_eval_cycles", "batch_scale_cycles", "batch_commit_cycles")
         return dict(zip(keys, (int(x) for x in out)))
 
     def launches(self):

@@ -609,6 +609,9 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   A.off_ARG = take((Stop + 1) * Lp);
   A.off_BD = take(A.split_stride * 2);
   A.off_CELL = take(3 * (maxCells + 1) * 4);
+  A.off_CRAW = take(K1e * Lp * 4);
+  A.off_NRAW = take(Lp * 4);
+  A.off_POFF = take(maxCells * 8);
   A.warp_bytes = o;
   const int64_t nunits = unit_end - unit_begin;
   CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
@@ -680,7 +683,7 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
     CK(dalloc(&c->d_cur, J));
     CK(dalloc(&c->d_free, 16));
     CK(dalloc(&c->d_total, 1));
-    CK(dalloc(&c->d_round_stats, 16));
+    CK(dalloc(&c->d_round_stats, 24));
   }
   std::vector<int32_t> fr(T);
   for (int t = 0; t < T; ++t) {
@@ -762,7 +765,7 @@ crius_status crius_round_stats(crius_ctx *c, int64_t *out16, void *stream) {
   if (!c->d_round_stats) return fail(CRIUS_ESTATE, "no round has run");
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemcpyAsync(out8, c->d_round_stats, 128, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out8, c->d_round_stats, 168, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return CRIUS_OK;
 }

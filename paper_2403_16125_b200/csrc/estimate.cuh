@@ -34,6 +34,7 @@ struct EstArgs {
   // per-warp shared-memory layout (byte offsets)
   int32_t Lp, K1e, Stop, maxCells;
   int32_t off_PC, off_PW, off_PA, off_PV, off_PN, off_BND, off_F, off_ARG, off_BD, off_CELL;
+  int32_t off_CRAW, off_NRAW, off_POFF;
   int32_t warp_bytes;
 };
 
@@ -121,6 +122,119 @@ __device__ __forceinline__ int64_t plan_time(const UnitCtx &U, int G, int S, int
   return sumT + (int64_t)((1ll << lB) - 1) * maxT + maxSync;
 }
 
+// ---- cp.async (LDGSTS) staging: global -> shared without registers ---------
+__device__ __forceinline__ void cp_async4(void *sdst, const void *gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// In-place inclusive prefix of x[1..L] (x[0] := 0); int64 entries in shared memory.
+__device__ __forceinline__ void warp_prefix_inplace(int64_t *x, int L, int lane) {
+  int64_t carry = 0;
+  for (int b = 0; b < L; b += 32) {
+    const int64_t v = (b + lane < L) ? x[b + lane + 1] : 0;
+    const int64_t inc = warp_incl_scan(v, lane);
+    __syncwarp();
+    if (b + lane < L) x[b + lane + 1] = carry + inc;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) x[0] = 0;
+}
+
+// Inclusive prefix of an int32 shared-memory row src[0..L) into dst[0..L].
+__device__ __forceinline__ void warp_prefix32(int64_t *dst, const int32_t *src, int L, int lane) {
+  int64_t carry = 0;
+  if (lane == 0) dst[0] = 0;
+  for (int b = 0; b < L; b += 32) {
+    const int64_t v = (b + lane < L) ? (int64_t)src[b + lane] : 0;
+    const int64_t inc = warp_incl_scan(v, lane);
+    if (b + lane < L) dst[b + lane + 1] = carry + inc;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+}
+
+// K2 rows f[2..smax] (lowest-argmin binary search, §N3), in the narrowest
+// integer type that holds P[L] (every f value is <= P[L]): exact either way.
+template <typename V>
+__device__ __forceinline__ void stage_dp(const V *P0, V *F0, V *F1, uint8_t *ARG, int Lp, int L,
+                                         int smax, int lane) {
+  for (int i = lane; i <= L; i += 32) F0[i] = P0[i];
+  __syncwarp();
+  V *fp = F0, *fc = F1;
+  for (int s = 2; s <= smax; ++s) {
+    uint8_t *arow = ARG + s * Lp;
+    for (int i = s + lane; i <= L; i += 32) {
+      const V Pi = P0[i];
+      int lo = s - 1, hi = i;  // first k in [s-1, i-1] with f[s-1][k] >= P[i]-P[k], else i
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (fp[mid] >= Pi - P0[mid])
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      int a;
+      V val;
+      if (lo == s - 1) {
+        a = lo;
+        val = fp[lo];
+      } else {
+        const V v0 = Pi - P0[lo - 1];  // value at k1-1 (its max is the stage term)
+        if (lo == i) {
+          a = lo - 1;
+          val = v0;
+        } else {
+          const V v1 = fp[lo];
+          if (v0 <= v1) {
+            a = lo - 1;
+            val = v0;
+          } else {
+            a = lo;
+            val = v1;
+          }
+        }
+      }
+      fc[i] = val;
+      arow[i] = (uint8_t)a;
+    }
+    __syncwarp();
+    V *tmp = fp;
+    fp = fc;
+    fc = tmp;
+  }
+}
+
+// Metadata of one unit, loaded one unit ahead (independent loads, one round trip).
+struct UnitMeta {
+  int64_t u, cb, ce, pb, pe, off;
+  int L, ng, gb, kst;
+};
+
+__device__ __forceinline__ UnitMeta load_meta(const Params &P, const EstArgs &A, int64_t u) {
+  UnitMeta m;
+  m.u = u;
+  if (u < A.unit_end) {
+    const int j = (int)(u / P.T);
+    m.cb = A.ucb[u];
+    m.ce = A.ucb[u + 1];
+    m.pb = A.upb[u];
+    m.pe = A.upb[u + 1];
+    m.off = P.off[j];
+    m.L = P.L[j];
+    m.ng = P.ng[j];
+    m.gb = P.gb[j];
+    m.kst = P.kst[j];
+  }
+  return m;
+}
+
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_estimate(Params P, EstArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -137,99 +251,88 @@ __global__ void __launch_bounds__(WARPS * 32) k_estimate(Params P, EstArgs A) {
   int16_t *BD = (int16_t *)(base + A.off_BD);
   int32_t *CG = (int32_t *)(base + A.off_CELL);
   int32_t *CS = CG + (A.maxCells + 1), *CP = CS + (A.maxCells + 1);
+  int32_t *CRAW = (int32_t *)(base + A.off_CRAW);  // [K1e][Lp] raw compute rows
+  int32_t *NRAW = (int32_t *)(base + A.off_NRAW);  // [Lp] raw tp_calls, then the int32 P0
+  int64_t *POFF = (int64_t *)(base + A.off_POFF);  // [maxCells] raw plan offsets
   const int Lp = A.Lp;
   const int64_t out_cell_base = A.ucb[A.unit_begin];
 
-  for (;;) {
-    int64_t u = 0;
-    if (lane == 0) u = A.unit_begin + atomicAdd(A.work_counter, 1);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= A.unit_end) break;
+  int64_t un = 0;
+  if (lane == 0) un = A.unit_begin + atomicAdd(A.work_counter, 1);
+  un = __shfl_sync(0xffffffffu, un, 0);
+  UnitMeta nm = load_meta(P, A, un);
 
-    const int j = (int)(u / P.T), t = (int)(u % P.T);
-    const int64_t cb = A.ucb[u];
-    const int nc = (int)(A.ucb[u + 1] - cb);
+  for (;;) {
+    const UnitMeta m = nm;
+    const int64_t u = m.u;
+    if (u >= A.unit_end) break;
+    // grab and prefetch the metadata of the next unit while this one runs
+    if (lane == 0) un = A.unit_begin + atomicAdd(A.work_counter, 1);
+    un = __shfl_sync(0xffffffffu, un, 0);
+    nm = load_meta(P, A, un);
+
+    const int t = (int)(u % P.T);
+    const int64_t cb = m.cb;
+    const int nc = (int)(m.ce - cb);
     int16_t *split_out = A.splits ? A.splits + (u - A.unit_begin) * A.split_stride : nullptr;
     if (nc == 0) {
       if (split_out)
         for (int q = lane; q < A.split_stride; q += 32) split_out[q] = -1;
       continue;
     }
-    const int64_t pb = A.upb[u];
-    const int npu = (int)(A.upb[u + 1] - pb);
-    const int L = P.L[j];
-    const int64_t off = P.off[j];
+    const int64_t pb = m.pb;
+    const int npu = (int)(m.pe - pb);
+    const int L = m.L;
+    const int64_t off = m.off;
+    // compute planes needed: k <= log2(max g), max g <= min(largest G of the unit, g_max)
+    const int cap = P.ty[t].cap;
+    const int gtop = P.gpu_set == 1 ? cap : (2 * m.ng <= cap ? 2 * m.ng : (m.ng <= cap ? m.ng : m.ng / 2));
+    const int K1s = min(ilog2_pow2(max(1, min(gtop, P.g_max))) + 1, A.K1e);
 
-    // ---- Cells of the unit -> shared memory
+    // ---- A3: stage every row of the unit with cp.async (one round trip), then scan
+    for (int k = 0; k < K1s; ++k) {
+      const int32_t *src = P.c + ((int64_t)t * P.K1 + k) * P.TL + off;
+      for (int l = lane; l < L; l += 32) cp_async4(CRAW + k * Lp + l, src + l);
+    }
+    for (int l = lane; l < L; l += 32) {
+      cp_async8(PW + l + 1, P.w + off + l);
+      cp_async8(PA + l + 1, P.act + off + l);
+      cp_async8(PV + l + 1, P.tpv + off + l);
+      cp_async8(BND + l, P.bnd + off + l);
+      cp_async4(NRAW + l, P.tpn + off + l);
+    }
+    for (int i = lane; i < nc; i += 32) {
+      cp_async4(CG + i, A.cG + cb + i);
+      cp_async4(CS + i, A.cS + cb + i);
+      cp_async8(POFF + i, A.plan_off + cb + i);
+    }
+    cp_async_wait_all();
+    __syncwarp();
     int smax = 0, gmax = 0;
     for (int i = lane; i < nc; i += 32) {
-      const int G = A.cG[cb + i], S = A.cS[cb + i];
-      CG[i] = G;
-      CS[i] = S;
-      CP[i] = (int)(A.plan_off[cb + i] - pb);
-      smax = max(smax, S);
-      gmax = max(gmax, G / S);
+      CP[i] = (int)(POFF[i] - pb);
+      smax = max(smax, CS[i]);
+      gmax = max(gmax, CG[i] / CS[i]);
     }
     if (lane == 0) CP[nc] = npu;
     smax = warp_max_int(smax);
     gmax = warp_max_int(gmax);
-    const int K1u = ilog2_pow2(gmax) + 1;
-
-    // ---- A3: prefix staging (HBM -> shared, once per unit)
-    for (int k = 0; k < K1u; ++k)
-      warp_prefix(PC + k * Lp, P.c + ((int64_t)t * P.K1 + k) * P.TL + off, L, lane);
-    warp_prefix(PW, P.w + off, L, lane);
-    warp_prefix(PA, P.act + off, L, lane);
-    warp_prefix(PV, P.tpv + off, L, lane);
-    warp_prefix(PN, P.tpn + off, L, lane);
-    for (int l = lane; l < L; l += 32) BND[l] = __ldg(P.bnd + off + l);
+    const int K1u = ilog2_pow2(gmax) + 1;  // <= K1s
+    for (int k = 0; k < K1u; ++k) warp_prefix32(PC + k * Lp, CRAW + k * Lp, L, lane);
+    warp_prefix_inplace(PW, L, lane);
+    warp_prefix_inplace(PA, L, lane);
+    warp_prefix_inplace(PV, L, lane);
+    warp_prefix32(PN, NRAW, L, lane);
     __syncwarp();
 
     // ---- K2: stage DP rows f[1..smax] over P0 = PC[0]
-    const int64_t *P0 = PC;
-    for (int i = lane; i <= L; i += 32) F0[i] = P0[i];
-    __syncwarp();
-    int64_t *fp = F0, *fc = F1;
-    for (int s = 2; s <= smax; ++s) {
-      uint8_t *arow = ARG + s * Lp;
-      for (int i = s + lane; i <= L; i += 32) {
-        const int64_t Pi = P0[i];
-        int lo = s - 1, hi = i;  // first k in [s-1, i-1] with f[s-1][k] >= P[i]-P[k], else i
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (fp[mid] >= Pi - P0[mid])
-            hi = mid;
-          else
-            lo = mid + 1;
-        }
-        int a;
-        int64_t val;
-        if (lo == s - 1) {
-          a = lo;
-          val = fp[lo];
-        } else {
-          const int64_t v0 = Pi - P0[lo - 1];  // value at k1-1 (its max is the stage term)
-          if (lo == i) {
-            a = lo - 1;
-            val = v0;
-          } else {
-            const int64_t v1 = fp[lo];
-            if (v0 <= v1) {
-              a = lo - 1;
-              val = v0;
-            } else {
-              a = lo;
-              val = v1;
-            }
-          }
-        }
-        fc[i] = val;
-        arow[i] = (uint8_t)a;
-      }
+    if (PC[L] < (int64_t)INT32_MAX) {
+      int32_t *P32 = NRAW;
+      for (int i = lane; i <= L; i += 32) P32[i] = (int32_t)PC[i];
       __syncwarp();
-      int64_t *tmp = fp;
-      fp = fc;
-      fc = tmp;
+      stage_dp<int32_t>(P32, (int32_t *)F0, (int32_t *)F0 + Lp, ARG, Lp, L, smax, lane);
+    } else {
+      stage_dp<int64_t>(PC, F0, F1, ARG, Lp, L, smax, lane);
     }
 
     // ---- R0 backtrack, one lane per S = 2^si
@@ -261,11 +364,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_estimate(Params P, EstArgs A) {
     U.BND = BND;
     U.BD = BD;
     U.Lp = Lp;
-    U.lGB = ilog2_pow2(P.gb[j]);
+    U.lGB = ilog2_pow2(m.gb);
     U.lgpn = P.ty[t].lgpn;
     U.b_mode = P.b_mode;
     U.nB = P.nB;
-    U.kst = P.kst[j];
+    U.kst = m.kst;
     U.memt = P.ty[t].mem;
     U.a_in = P.ty[t].a_in;
     U.b_in = P.ty[t].b_in;

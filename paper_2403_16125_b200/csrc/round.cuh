@@ -134,8 +134,15 @@ struct JobWin {
 
 struct RoundShared {
   int32_t fr[kRT];
-  int32_t n_adm, seq_valid, advance, any_change, n_dirty, n_list;
-  long long prof[8];  // cycles: [0] setup+dirty, [1] (i) pass, [2] (ii) pass, [3] reduce+apply; [4] dirty jobs, [5] listed jobs
+  int32_t n_adm, advance, any_change, n_dirty, n_list, n_invalid;
+  // per-type sequence validity: a sequence is reused until a job of its type
+  // changes or a changed free count could admit an other-type move of one of its
+  // jobs (gmin_type = smallest option G over its jobs, a conservative bound)
+  int32_t seq_ok[kRT], comp[kRT], gmin_type[kRT];
+  int32_t fr_base[kRT][kRT];  // free counts the sequence was computed from
+  int32_t old_fr[kRT];        // free counts before the current commit (thread 0)
+  uint32_t changed;           // types changed by the current commit; 0 = no commit
+  long long prof[12];  // cycles: [0] setup+dirty, [1] (i) pass, [2] (ii) pass, [3] reduce+apply; [4] dirty jobs, [5] listed jobs
   // victim-move sequences, one per GPU type, cut at <= d moves
   int32_t len[kRT], active[kRT];
   int32_t mv_a[kRT][kMaxDepth], mv_opt[kRT][kMaxDepth];
@@ -296,15 +303,23 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int TT = R.T, n_adm = sh.n_adm;
   if (tid < TT) {
-    sh.len[tid] = 0;
-    sh.active[tid] = 1;
-    sh.cum[tid][0] = 0.0;
-    int fm = -1;
-    for (int q = 0; q < TT; ++q)
-      if (q != tid) fm = max(fm, sh.fr[q]);
-    sh.fmax_other[tid] = fm;
+    const int c = !sh.seq_ok[tid];
+    sh.comp[tid] = c;
+    sh.active[tid] = c;
+    if (c) {
+      sh.len[tid] = 0;
+      sh.cum[tid][0] = 0.0;
+      sh.gmin_type[tid] = INT32_MAX;
+      int fm = -1;
+      for (int q = 0; q < TT; ++q)
+        if (q != tid) fm = max(fm, sh.fr[q]);
+      sh.fmax_other[tid] = fm;
+    }
   }
-  if (tid < TT * TT) sh.frs[tid / TT][0][tid % TT] = sh.fr[tid % TT];
+  if (tid < TT * TT && !sh.seq_ok[tid / TT]) {
+    sh.frs[tid / TT][0][tid % TT] = sh.fr[tid % TT];
+    sh.fr_base[tid / TT][tid % TT] = sh.fr[tid % TT];
+  }
   if (lane < TT) sh.r_a[lane][wid] = -1;
   if (tid == 0) sh.n_dirty = 0;
   long long t0 = clock64();
@@ -331,6 +346,7 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
       int myt = -1;
       if (a < n_adm) {
         myt = A.t[a];
+        if (m == 0 && sh.comp[myt]) atomicMin(&sh.gmin_type[myt], A.gmin[a]);
         bool moved = !sh.active[myt];
         for (int q = 0; q < m; ++q) moved |= sh.mv_a[myt][q] == a;
         if (!moved) {
@@ -402,8 +418,24 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
       t0 = t1;
     }
   }
-  if (tid == 0) sh.seq_valid = 1;
+  if (tid < TT && sh.comp[tid]) sh.seq_ok[tid] = 1;
   __syncthreads();
+}
+
+// Warp 0 after a commit (lane t checks type t): drop the sequences the commit
+// can have changed.  sh.changed = types whose job set or a job's option changed;
+// sh.old_fr = free counts before the commit.
+__device__ __forceinline__ void invalidate_seqs(RoundShared &sh, int TT) {
+  const int t = threadIdx.x & 31;
+  if (t >= TT || !sh.seq_ok[t]) return;
+  bool bad = (sh.changed >> t) & 1;
+  for (int q = 0; q < TT && !bad; ++q)
+    if (q != t && sh.old_fr[q] != sh.fr[q] && sh.gmin_type[t] <= max(sh.old_fr[q], sh.fr[q]))
+      bad = true;
+  if (bad) {
+    sh.seq_ok[t] = 0;
+    atomicAdd(&sh.n_invalid, 1);
+  }
 }
 
 // Warp-wide argmin of kappa over `nopt` option records passing `pred` -> index or -1.
@@ -501,16 +533,24 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
   if (tid < TT) sh.fr[tid] = R.free_io[tid];
   if (tid == 0) {
     sh.n_adm = 0;
-    sh.seq_valid = 0;
+    sh.n_invalid = 0;
   }
-  if (tid < 8) sh.prof[tid] = 0;
+  if (tid < kRT) sh.seq_ok[tid] = 0;
+  if (tid == 0) sh.changed = 0;
+  if (tid < 12) sh.prof[tid] = 0;
   __syncthreads();
   long long c_start = clock64(), c_seq = 0, n_batches = 0, n_seq = 0, n_scale = 0, n_bb = 0;
   load_window(W, R, 0);
 
   // ---- Phase A: SchedArrival in priority order
+  long long tb = clock64();
   for (int pos0 = 0; pos0 < R.J;) {
     if (pos0 + kRoundWarps > W.w0 + W.wn && W.w0 + W.wn < R.J) load_window(W, R, pos0);
+    if (tid == 0) {
+      const long long t1 = clock64();
+      sh.prof[8] += t1 - tb;
+      tb = t1;
+    }
     const int q = pos0 + wid, wq = q - W.w0;
     int kind = 0, opt = -1, need = 0;
     if (q < R.J && W.ref[wq] != kInf) {
@@ -533,11 +573,18 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
     }
     __syncthreads();
     ++n_batches;
+    if (tid == 0) {
+      const long long t1 = clock64();
+      sh.prof[9] += t1 - tb;
+      tb = t1;
+    }
     const unsigned kmask = __ballot_sync(0xffffffffu, sh.res_kind[lane] != 0);
     const int fa = kmask ? __ffs(kmask) - 1 : kRoundWarps;
     const unsigned nmask = __ballot_sync(0xffffffffu, lane < fa && sh.need[lane]);
     if (nmask) {
-      if (!sh.seq_valid) {
+      bool stale = false;
+      for (int q = 0; q < TT; ++q) stale |= !sh.seq_ok[q];
+      if (stale) {
         const long long c0 = clock64();
         compute_all_seqs(sh, R, A, list);
         c_seq += clock64() - c0;
@@ -555,7 +602,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
           const int len = sh.len[x.t];
           int m = -1;
           for (int mm = 0; mm <= len; ++mm)
-            if (x.G <= sh.frs[x.t][mm][x.t]) {
+            if (x.G <= sh.frs[x.t][mm][x.t] - sh.fr_base[x.t][x.t] + sh.fr[x.t]) {
               m = mm;
               break;
             }
@@ -577,34 +624,82 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       }
       __syncthreads();
     }
+    if (tid == 0) {
+      const long long t1 = clock64();
+      sh.prof[10] += t1 - tb;
+      tb = t1;
+    }
     if (tid < 32) {
       const unsigned fmask = __ballot_sync(0xffffffffu, sh.res_kind[lane] != 0);
       const int f = fmask ? __ffs(fmask) - 1 : kRoundWarps;
-      if (tid == 0 && f < kRoundWarps) {
-        const int pos = pos0 + f, oi = sh.res_opt[f];
-        const OptRec x = W.opt[(size_t)(pos - W.w0) * R.maxopt + oi];
-        if (sh.res_kind[f] == 2) {
-          ++n_scale;
-          const int m = sh.res_m[f], t = x.t;
-          for (int mm = 0; mm < m; ++mm) {
-            const int a = sh.mv_a[t][mm];
-            adm_set(A, R, a, A.pos[a], sh.mv_opt[t][mm], sh.mv_G[t][mm], sh.mv_t[t][mm],
-                    sh.mv_T[t][mm], sh.mv_sc[t][mm]);
+      if (tid == 0) {
+        int adv = kRoundWarps;
+        if (f < kRoundWarps) {
+          const int pos = pos0 + f, oi = sh.res_opt[f];
+          const OptRec x = W.opt[(size_t)(pos - W.w0) * R.maxopt + oi];
+          int32_t *old_fr = sh.old_fr;
+          for (int qq = 0; qq < TT; ++qq) old_fr[qq] = sh.fr[qq];
+          unsigned changed = 1u << 31;  // bit 31: a commit happened
+          if (sh.res_kind[f] == 2) {
+            ++n_scale;
+            const int m = sh.res_m[f], t = x.t;
+            for (int mm = 0; mm < m; ++mm) {
+              const int a = sh.mv_a[t][mm];
+              changed |= (1u << A.t[a]) | (1u << sh.mv_t[t][mm]);
+              adm_set(A, R, a, A.pos[a], sh.mv_opt[t][mm], sh.mv_G[t][mm], sh.mv_t[t][mm],
+                      sh.mv_T[t][mm], sh.mv_sc[t][mm]);
+            }
+            for (int qq = 0; qq < TT; ++qq)
+              sh.fr[qq] = sh.frs[t][m][qq] - sh.fr_base[t][qq] + old_fr[qq];
           }
-          for (int qq = 0; qq < TT; ++qq) sh.fr[qq] = sh.frs[t][m][qq];
+          const int kind0 = sh.res_kind[f];
+          int w = f;
+          for (;;) {  // commit job w (admitted directly, or the first job's scale result)
+            const int wq0 = pos0 + w - W.w0, o = sh.res_opt[w];
+            const OptRec y = W.opt[(size_t)wq0 * R.maxopt + o];
+            sh.fr[y.t] -= y.G;
+            changed |= 1u << y.t;
+            const int na = sh.n_adm;
+            adm_set(A, R, na, pos0 + w, o, y.G, y.t, y.T, W.score[(size_t)wq0 * R.maxopt + o]);
+            A.nopt[na] = W.nopt[wq0];
+            sh.n_adm += 1;
+            adv = w + 1;
+            if (kind0 != 1) break;
+            // A direct admission only lowers one free count, so a later job's
+            // direct choice stands iff its option still fits; a job that stays
+            // pending/unschedulable without ScaleResource is unaffected.
+            bool more = false;
+            while (++w < kRoundWarps && pos0 + w < R.J) {
+              const int kw = sh.res_kind[w];
+              if (kw == 1) {
+                const OptRec z = W.opt[(size_t)(pos0 + w - W.w0) * R.maxopt + sh.res_opt[w]];
+                more = z.G <= sh.fr[z.t];
+                break;
+              }
+              if (kw == 0 && !sh.need[w]) {
+                adv = w + 1;
+                continue;
+              }
+              break;
+            }
+            if (!more) break;
+          }
+          sh.changed = changed;
         }
-        sh.fr[x.t] -= x.G;
-        const int wq0 = pos - W.w0;
-        const int na = sh.n_adm;
-        adm_set(A, R, na, pos, oi, x.G, x.t, x.T, W.score[(size_t)wq0 * R.maxopt + oi]);
-        A.nopt[na] = W.nopt[wq0];
-        sh.n_adm += 1;
-        sh.seq_valid = 0;
+        sh.advance = adv;
       }
-      if (tid == 0) sh.advance = f < kRoundWarps ? f + 1 : kRoundWarps;
+      __syncwarp();
+      if (sh.changed) invalidate_seqs(sh, TT);
+      __syncwarp();
+      if (tid == 0) sh.changed = 0;
     }
     __syncthreads();
     pos0 += sh.advance;
+    if (tid == 0) {
+      const long long t1 = clock64();
+      sh.prof[11] += t1 - tb;
+      tb = t1;
+    }
   }
 
   // ---- Phase B: up to d sweeps of reverse scaling over admitted jobs
@@ -673,6 +768,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       R.stats[6] = n_scale;
       R.stats[7] = n_bb;
       for (int q = 0; q < 6; ++q) R.stats[8 + q] = sh.prof[q];
+      R.stats[14] = sh.n_invalid;
+      for (int q = 8; q < 12; ++q) R.stats[7 + q] = sh.prof[q];
     }
   }
   __syncthreads();
