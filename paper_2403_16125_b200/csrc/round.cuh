@@ -380,9 +380,10 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
     }
     if (wid < TT && sh.active[wid]) {  // warp t reduces type t, applies its move, preps m+1
       const int t = wid;
-      const int ra = sh.r_a[t][lane];
-      const int src = warp_lex_argmin(ra >= 0, ord_double(sh.r_key[t][lane]),
-                                      ((uint32_t)ra << 8) | (uint32_t)sh.r_i[t][lane]);
+      const bool in = lane < kRoundWarps;
+      const int ra = in ? sh.r_a[t][lane] : -1;
+      const int src = warp_lex_argmin(ra >= 0, ord_double(in ? sh.r_key[t][lane] : 0.0),
+                                      ((uint32_t)ra << 8) | (uint32_t)(in ? sh.r_i[t][lane] : 0));
       if (src < 0) {
         if (lane == 0) sh.active[t] = 0;
       } else {
@@ -408,7 +409,7 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
           sh.len[t] = m + 1;
         }
         __syncwarp();
-        sh.r_a[t][lane] = -1;  // reset this type's slots for move m + 1
+        if (lane < kRoundWarps) sh.r_a[t][lane] = -1;  // reset this type's slots for move m + 1
       }
     }
     __syncthreads();
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       sh.prof[9] += t1 - tb;
       tb = t1;
     }
-    const unsigned kmask = __ballot_sync(0xffffffffu, sh.res_kind[lane] != 0);
+    const unsigned kmask = __ballot_sync(0xffffffffu, lane < kRoundWarps && sh.res_kind[lane] != 0);
     const int fa = kmask ? __ffs(kmask) - 1 : kRoundWarps;
     const unsigned nmask = __ballot_sync(0xffffffffu, lane < fa && sh.need[lane]);
     if (nmask) {
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       tb = t1;
     }
     if (tid < 32) {
-      const unsigned fmask = __ballot_sync(0xffffffffu, sh.res_kind[lane] != 0);
+      const unsigned fmask = __ballot_sync(0xffffffffu, lane < kRoundWarps && sh.res_kind[lane] != 0);
       const int f = fmask ? __ffs(fmask) - 1 : kRoundWarps;
       if (tid == 0) {
         int adv = kRoundWarps;
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       }
       __syncthreads();
       if (tid < 32) {
-        const unsigned fmask = __ballot_sync(0xffffffffu, sh.res_opt[lane] >= 0);
+        const unsigned fmask = __ballot_sync(0xffffffffu, lane < kRoundWarps && sh.res_opt[lane] >= 0);
         const int f = fmask ? __ffs(fmask) - 1 : kRoundWarps;
         if (tid == 0 && f < kRoundWarps) {
           const int aa = a0 + f;
