@@ -23,7 +23,7 @@ import numpy as np
 from . import workload  # noqa: F401  (seeded inputs; none of the method's arithmetic)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcrius.so")
+LIB_PATH = os.environ.get("CRIUS_LIB") or os.path.join(HERE, "libcrius.so")
 INF = np.iinfo(np.int64).max
 RECORD_BYTES = 16
 

@@ -612,6 +612,7 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   A.off_CRAW = take(K1e * Lp * 4);
   A.off_NRAW = take(Lp * 4);
   A.off_POFF = take(maxCells * 8);
+  A.off_ORD = take((maxCells + 1) * 4);
   A.warp_bytes = o;
   const int64_t nunits = unit_end - unit_begin;
   CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
@@ -619,21 +620,21 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   if (4 * A.warp_bytes > 200 * 1024) warps = 1;
   if (A.warp_bytes > 220 * 1024) return fail(CRIUS_EINVAL, "unit too large for shared memory");
   const size_t smem = (size_t)warps * A.warp_bytes;
+  // one lane per (Cell, k, group of microbatch counts): 1 B per lane (B = 4S)
+  // or up to 8 of the configured B values per lane
+  const bool wide = c->P.b_mode == 1;
+#ifndef CRIUS_NBG_WIDE
+#define CRIUS_NBG_WIDE 4  // microbatch counts per lane in b_mode 1 (measured best)
+#endif
+  auto kern = warps == 4 ? (wide ? k_estimate<4, CRIUS_NBG_WIDE> : k_estimate<4, 1>)
+                         : (wide ? k_estimate<1, CRIUS_NBG_WIDE> : k_estimate<1, 1>);
   int per_sm = 1;
-  if (warps == 4) {
-    CK(cudaFuncSetAttribute(k_estimate<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_estimate<4>, 128, smem));
-  } else {
-    CK(cudaFuncSetAttribute(k_estimate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_estimate<1>, 32, smem));
-  }
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
   per_sm = std::max(per_sm, 1);
   const int64_t want = (nunits + warps - 1) / warps;
   const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)c->n_sm * per_sm);
-  if (warps == 4)
-    k_estimate<4><<<grid, 128, smem, st>>>(c->P, A);
-  else
-    k_estimate<1><<<grid, 32, smem, st>>>(c->P, A);
+  kern<<<grid, 32 * warps, smem, st>>>(c->P, A);
   CKL();
   c->launches += 1;
   return CRIUS_OK;

@@ -34,7 +34,7 @@ struct EstArgs {
   // per-warp shared-memory layout (byte offsets)
   int32_t Lp, K1e, Stop, maxCells;
   int32_t off_PC, off_PW, off_PA, off_PV, off_PN, off_BND, off_F, off_ARG, off_BD, off_CELL;
-  int32_t off_CRAW, off_NRAW, off_POFF;
+  int32_t off_CRAW, off_NRAW, off_POFF, off_ORD;
   int32_t warp_bytes;
 };
 
@@ -120,6 +120,127 @@ __device__ __forceinline__ int64_t plan_time(const UnitCtx &U, int G, int S, int
     pa_a = pa_e;
   }
   return sumT + (int64_t)((1ll << lB) - 1) * maxT + maxSync;
+}
+
+// ceil((hi:lo) / 2^e) for a 128-bit value whose result fits 64 bits; e <= 0
+// means an exact left shift of the low word.
+__device__ __forceinline__ uint64_t ceil_shr128(uint64_t hi, uint64_t lo, int e) {
+  if (e <= 0) return lo << (-e);
+  const uint64_t add = (1ull << e) - 1;
+  const uint64_t lo2 = lo + add;
+  hi += (lo2 < lo);
+  return (hi << (64 - e)) | (lo2 >> e);
+}
+
+// T_iter of every microbatch count of one (Cell, k) group at once (§N5).  The
+// per-stage memory filter and DP sync do not depend on B; mb = GB/(B dp) = 2^lmb,
+// so every alpha-beta term is a 128-bit product formed once per stage (tpc: X,
+// boundary send: Y, boundary all-gather: Z) followed, per B, by an exact
+// ceil-shift.  Returns the best (T, p) of the group (lowest p on ties).
+template <int NBG>
+__device__ __forceinline__ int64_t plan_group_time(const UnitCtx &U, int G, int S, int k, int bg,
+                                                   int &best_p) {
+  const int lS = ilog2_pow2(S), lg = ilog2_pow2(G) - lS;
+  const int ldp = lg - k;
+  int lB[NBG], lmb[NBG];
+  bool ok[NBG];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < NBG; ++q) {
+    const int b = bg * NBG + q;
+    lB[q] = U.b_mode == 0 ? lS + 2 : (b < U.nB ? U.lBv[b] : 0);
+    lmb[q] = U.lGB - lB[q] - ldp;
+    ok[q] = (U.b_mode == 0 ? q == 0 : b < U.nB) && lmb[q] >= 0;  // B dp <= GB (A-12)
+    any |= ok[q];
+  }
+  if (!any) return kInf;
+  const uint64_t tp = 1ull << k, dp = 1ull << ldp;
+  const bool tp_in = k <= U.lgpn, dp_in = lg <= U.lgpn;  // A-15
+  const uint64_t a_tp = tp_in ? U.a_in : U.a_x, b_tp = tp_in ? U.b_in : U.b_x;
+  const uint64_t a_dp = dp_in ? U.a_in : U.a_x, b_dp = dp_in ? U.b_in : U.b_x;
+  const int64_t *PCk = U.PC + k * U.Lp;
+  const int16_t *bd = U.BD + (S - 1) + lS;
+  const int node_mask = lg < U.lgpn ? (1 << (U.lgpn - lg)) - 1 : 0;
+  int64_t sumT[NBG], maxT[NBG];
+#pragma unroll
+  for (int q = 0; q < NBG; ++q) sumT[q] = maxT[q] = 0;
+  int64_t maxSync = 0;
+  int a = 0;
+  int64_t pc_a = 0, pv_a = 0, pn_a = 0, pw_a = 0, pa_a = 0;
+  for (int s = 0; s < S; ++s) {
+    const int e = bd[s + 1];
+    const int64_t pc_e = PCk[e], pv_e = U.PV[e], pn_e = U.PN[e], pw_e = U.PW[e], pa_e = U.PA[e];
+    const int64_t W = pw_e - pw_a, A = pa_e - pa_a, C = pc_e - pc_a;
+    // mem = cdiv(kst W + (GB/dp) A, tp) <= mem_t  (A-13): B-independent
+    const uint64_t mem = ((uint64_t)(U.kst * W + (A << (U.lGB - ldp))) + tp - 1) >> k;
+    if (mem > (uint64_t)U.memt) return kInf;
+    // sync = AR(dp, l_dp, cdiv(W, tp), 1): B-independent
+    if (ldp) {
+      const uint64_t Wt = ((uint64_t)W + tp - 1) >> k;
+      const uint64_t sy = 2 * (dp - 1) * a_dp + mul_shr_ceil(2 * (dp - 1) * Wt, b_dp, ldp + 20);
+      maxSync = max(maxSync, (int64_t)sy);
+    }
+    // tpc = N 2(tp-1) alpha + ceil(X 2^lmb / 2^(k+20)),  X = 2(tp-1) TPV beta
+    uint64_t Xh = 0, Xl = 0, tpn_alpha = 0;
+    if (k) {
+      const uint64_t x = 2 * (tp - 1) * (uint64_t)(pv_e - pv_a);
+      Xl = x * b_tp;
+      Xh = __umul64hi(x, b_tp);
+      tpn_alpha = (uint64_t)(pn_e - pn_a) * (2 * (tp - 1)) * a_tp;
+    }
+    // inb = P2P(l_b, cdiv(mb bnd, tp)) + AG(tp, l_tp, mb bnd):  Y = bnd beta_b, Z = (tp-1) bnd beta_tp
+    uint64_t Yh = 0, Yl = 0, Zh = 0, Zl = 0, a_b = 0, b_b = 0, bnd = 0;
+    if (s) {
+      bnd = (uint64_t)U.BND[a - 1];
+      const bool b_in = (s & node_mask) != 0;
+      a_b = b_in ? U.a_in : U.a_x;
+      b_b = b_in ? U.b_in : U.b_x;
+      Yl = bnd * b_b;
+      Yh = __umul64hi(bnd, b_b);
+      if (k) {
+        const uint64_t z = (tp - 1) * bnd;
+        Zl = z * b_tp;
+        Zh = __umul64hi(z, b_tp);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NBG; ++q) {
+      if (!ok[q]) continue;
+      const int lm = lmb[q];
+      uint64_t T = (uint64_t)C << lm;
+      if (k) T += tpn_alpha + ceil_shr128(Xh, Xl, k + 20 - lm);
+      if (s) {
+        if (lm >= k) {
+          T += a_b + ceil_shr128(Yh, Yl, 20 - (lm - k));
+        } else {
+          const int sh = k - lm;
+          T += a_b + mul_shr_ceil((bnd + (1ull << sh) - 1) >> sh, b_b, 20);
+        }
+        if (k) T += (tp - 1) * a_tp + ceil_shr128(Zh, Zl, k + 20 - lm);
+      }
+      sumT[q] += (int64_t)T;
+      maxT[q] = max(maxT[q], (int64_t)T);
+    }
+    a = e;
+    pc_a = pc_e;
+    pv_a = pv_e;
+    pn_a = pn_e;
+    pw_a = pw_e;
+    pa_a = pa_e;
+  }
+  int64_t best = kInf;
+  int bq = 0;
+#pragma unroll
+  for (int q = 0; q < NBG; ++q) {
+    if (!ok[q]) continue;
+    const int64_t ti = sumT[q] + (int64_t)((1ll << lB[q]) - 1) * maxT[q] + maxSync;
+    if (ti < best) {
+      best = ti;
+      bq = q;
+    }
+  }
+  best_p = U.b_mode == 0 ? k : k * U.nB + bg * NBG + bq;
+  return best;
 }
 
 // ---- cp.async (LDGSTS) staging: global -> shared without registers ---------
@@ -235,8 +356,11 @@ __device__ __forceinline__ UnitMeta load_meta(const Params &P, const EstArgs &A,
   return m;
 }
 
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_estimate(Params P, EstArgs A) {
+#ifndef CRIUS_EST_MINB
+#define CRIUS_EST_MINB 4  // <= 128 registers: 4 CTAs (16 warps) per SM
+#endif
+template <int WARPS, int NBG>
+__global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params P, EstArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned char *base = smem + (size_t)wid * A.warp_bytes;
@@ -254,6 +378,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_estimate(Params P, EstArgs A) {
   int32_t *CRAW = (int32_t *)(base + A.off_CRAW);  // [K1e][Lp] raw compute rows
   int32_t *NRAW = (int32_t *)(base + A.off_NRAW);  // [Lp] raw tp_calls, then the int32 P0
   int64_t *POFF = (int64_t *)(base + A.off_POFF);  // [maxCells] raw plan offsets
+  int32_t *ORD = (int32_t *)(base + A.off_ORD);    // [maxCells] processing order (S desc)
   const int Lp = A.Lp;
   const int64_t out_cell_base = A.ucb[A.unit_begin];
 
@@ -376,15 +501,47 @@ __global__ void __launch_bounds__(WARPS * 32) k_estimate(Params P, EstArgs A) {
     U.b_x = P.ty[t].b_x;
     U.lBv = P.lB;
 
-    int carry_ci = -1, carry_p = 0;
+    // processing order: Cells by S descending (stable) so a 32-lane chunk runs
+    // stage loops of one length; item = (Cell, k, group of NBG microbatch counts)
+    const int ngrp = P.b_mode == 0 ? 1 : (P.nB + NBG - 1) / NBG;
+    const bool sorted = npu / P.nB * ngrp > 32;  // one chunk: order does not matter
+    for (int i = lane; i < nc; i += 32) {
+      int r = i;
+      if (sorted) {
+        const int si = CS[i];
+        r = 0;
+        for (int q = 0; q < nc; ++q) r += CS[q] > si || (CS[q] == si && q < i);
+      }
+      ORD[r] = i;
+    }
+    __syncwarp();
+    {
+      int64_t carry = 0;
+      for (int b0 = 0; b0 < nc; b0 += 32) {
+        const int r = b0 + lane;
+        int cnt = 0;
+        if (r < nc) {
+          const int ci = ORD[r];
+          cnt = (ilog2_pow2(CG[ci] / CS[ci]) + 1) * ngrp;
+        }
+        const int64_t inc = warp_incl_scan((int64_t)cnt, lane);
+        if (r < nc) CP[r + 1] = (int)(carry + inc);
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) CP[0] = 0;
+    }
+    __syncwarp();
+    const int nitems = CP[nc];
+
+    int carry_r = -1, carry_p = 0;
     int64_t carry_T = kInf;
-    for (int f0 = 0; f0 < npu; f0 += 32) {
+    for (int f0 = 0; f0 < nitems; f0 += 32) {
       const int f = f0 + lane;
-      const bool valid = f < npu;
-      int ci = nc, p = 0;
+      const bool valid = f < nitems;
+      int r = nc, p = 0;
       int64_t T = kInf;
       if (valid) {
-        int lo = 0, hi = nc - 1;  // largest ci with CP[ci] <= f
+        int lo = 0, hi = nc - 1;  // largest r with CP[r] <= f
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
           if (CP[mid] <= f)
@@ -392,45 +549,51 @@ __global__ void __launch_bounds__(WARPS * 32) k_estimate(Params P, EstArgs A) {
           else
             hi = mid - 1;
         }
-        ci = lo;
-        p = f - CP[ci];
-        T = plan_time(U, CG[ci], CS[ci], p);
+        r = lo;
+        const int ci = ORD[r], local = f - CP[r];
+        const int kk = NBG == 1 ? local : local / ngrp, gg = NBG == 1 ? 0 : local - kk * ngrp;
+        if (NBG == 1) {  // one microbatch count per lane: the per-plan evaluation
+          p = P.b_mode == 0 ? kk : kk * P.nB + gg;
+          T = plan_time(U, CG[ci], CS[ci], p);
+        } else {
+          T = plan_group_time<NBG>(U, CG[ci], CS[ci], kk, gg, p);
+        }
       }
       // segmented inclusive min-scan over (T, p); left lanes have lower p
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const int64_t oT = __shfl_up_sync(0xffffffffu, T, d);
         const int op = __shfl_up_sync(0xffffffffu, p, d);
-        const int oc = __shfl_up_sync(0xffffffffu, ci, d);
-        if (lane >= d && oc == ci && oT <= T) {
+        const int orr = __shfl_up_sync(0xffffffffu, r, d);
+        if (lane >= d && orr == r && oT <= T) {
           T = oT;
           p = op;
         }
       }
-      const int next_ci = __shfl_down_sync(0xffffffffu, ci, 1);
-      const bool tail = valid && (lane == 31 || next_ci != ci);
-      if (tail && ci == carry_ci && carry_T <= T) {
+      const int next_r = __shfl_down_sync(0xffffffffu, r, 1);
+      const bool tail = valid && (lane == 31 || next_r != r);
+      if (tail && r == carry_r && carry_T <= T) {
         T = carry_T;
         p = carry_p;
       }
-      const bool done = valid && (f + 1 == CP[ci + 1]);
+      const bool done = valid && (f + 1 == CP[r + 1]);
       if (tail && done) {
-        CellResult r;
-        r.t_ns = T;
-        r.plan = T == kInf ? -1 : p;
-        r.flags = T == kInf ? 0 : 1;
-        A.out[cb + ci - out_cell_base] = r;
+        CellResult res;
+        res.t_ns = T;
+        res.plan = T == kInf ? -1 : p;
+        res.flags = T == kInf ? 0 : 1;
+        A.out[cb + ORD[r] - out_cell_base] = res;
       }
-      const int c31 = __shfl_sync(0xffffffffu, ci, 31);
+      const int r31 = __shfl_sync(0xffffffffu, r, 31);
       const int64_t T31 = __shfl_sync(0xffffffffu, T, 31);
       const int p31 = __shfl_sync(0xffffffffu, p, 31);
       const bool open31 = __shfl_sync(0xffffffffu, (int)(valid && !done), 31);
       if (open31) {
-        carry_ci = c31;
+        carry_r = r31;
         carry_T = T31;
         carry_p = p31;
       } else {
-        carry_ci = -1;
+        carry_r = -1;
         carry_T = kInf;
       }
     }
