@@ -51,13 +51,17 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--assembly", type=int, default=0,
+                    help="NEXT-1: 1 = per-stage DP-only/TP-only (paper), 2 = every factorisation")
+    ap.add_argument("--form", type=int, default=1, help="pipeline form for --assembly (1 = paper)")
     return ap.parse_args()
 
 
 def workload_name(a):
     v = f"-{a.variant}" if a.variant else ""
     s = f"x{a.scale}" if a.scale != 1 else ""
-    return f"cfg{a.config}{v}{s}"
+    m = f"-assembly{a.assembly}form{a.form}" if getattr(a, "assembly", 0) else ""
+    return f"cfg{a.config}{v}{s}{m}"
 
 
 def config_dict(a, pr, n_cells, n_plans, world, flush):
@@ -270,7 +274,10 @@ def main():
         if world > 1:
             sharded.ShardPlan(cr, world)  # partition is part of the step (a tiny kernel + D2H)
         e1.record(stream)
-        cr.estimate(int(ub[rank]), int(ub[rank + 1]), out=mine)
+        if a.assembly:
+            cr.estimate_assembled(a.assembly, a.form, int(ub[rank]), int(ub[rank + 1]), out=mine)
+        else:
+            cr.estimate(int(ub[rank]), int(ub[rank + 1]), out=mine)
         e2.record(stream)
         if world > 1:
             dist.all_gather_into_tensor(gathered, mine[:plan.chunk])

@@ -158,6 +158,33 @@ crius_status crius_partition_units(crius_ctx *ctx, int32_t world, int64_t *unit_
 crius_status crius_estimate_cells(crius_ctx *ctx, int64_t unit_begin, int64_t unit_end,
                                   crius_cell_result *d_out, int16_t *d_splits, void *stream);
 
+/* NEXT-1: per-stage parallelism assembly -- the paper's own
+ * sampling, where each stage picks its parallelism independently ("assemble
+ * 2^{N_S} distinct parallelism plans") -- with either pipeline
+ * latency form.  Same Cells, splits and B set as crius_estimate_cells. */
+typedef struct {
+  int32_t mode;          /* 1 = each stage DP-only or TP-only (2^S plans);
+                            2 = every DP x TP factorisation per stage */
+  int32_t pipeline_form; /* 0 = sum + (B-1) max T (north_star);
+                            1 = sum + (B-1)(T_s* - T_comm,s*), s* = first slowest stage,
+                                T_comm its inbound communication */
+} crius_assembly;
+
+/* Exact best assembled plan of every Cell of units [unit_begin, unit_end)
+ * (no enumeration of the 2^S / K^S plans: threshold search over the slowest
+ * stage and the sync bound).  d_out[i]: t_ns = best latency, plan = index of
+ * the best microbatch count (B = 4S: 0), flags bit 0 = feasible.  d_stage_tp
+ * (optional DEVICE int8 buffer): per Cell crius_split_stride-independent row of
+ * max_S entries = log2 tp of each stage in one optimal plan, -1 padding
+ * (several plans can be optimal; any returned one attains t_ns).  max_S is the
+ * largest S of the enumeration (crius_max_stages).  Asynchronous. */
+crius_status crius_estimate_assembled(crius_ctx *ctx, const crius_assembly *assembly,
+                                      int64_t unit_begin, int64_t unit_end,
+                                      crius_cell_result *d_out, int8_t *d_stage_tp, void *stream);
+
+/* Largest stage count S of the enumerated Cells (row length of d_stage_tp). */
+int32_t crius_max_stages(const crius_ctx *ctx);
+
 /* Undo per-rank padding after an all-gather: d_gathered holds `world` chunks of
  * `chunk_stride` records, chunk r = Cells [cell_begin[r], cell_begin[r+1]) (host
  * array from crius_partition_units); writes d_all[n_cells].  Asynchronous. */

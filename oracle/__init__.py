@@ -132,6 +132,26 @@ class Oracle:
                     "estimate")
         return t_ns, plan
 
+    def estimate_assembled(self, cells, mode, form, c0=0, c1=None, kstride=None):
+        n = len(cells["job"])
+        c1 = n if c1 is None else c1
+        kstride = int(cells["S"].max()) if kstride is None else kstride
+        t_ns = np.zeros(c1 - c0, np.int64)
+        bidx = np.zeros(c1 - c0, np.int32)
+        sk = np.zeros((c1 - c0) * kstride, np.int8)
+        self._check(self.L.oracle_estimate_assembled(
+            C.byref(self.s), mode, form, *[_ptr(cells[k]) for k in ("job", "type", "G", "S")],
+            C.c_int64(c0), C.c_int64(c1), _ptr(t_ns), _ptr(bidx), _ptr(sk), kstride),
+            "estimate_assembled")
+        return t_ns, bidx, sk.reshape(c1 - c0, kstride)
+
+    def assembled_cost(self, form, j, t, G, S, bi, stage_k):
+        ks = np.ascontiguousarray(stage_k[:S], np.int8)
+        lat, fe = C.c_int64(), C.c_int32()
+        self._check(self.L.oracle_assembled_cost(C.byref(self.s), form, j, t, G, S, bi, _ptr(ks),
+                                                 C.byref(lat), C.byref(fe)), "assembled_cost")
+        return lat.value, bool(fe.value)
+
     def round(self, cells, t_ns, free_in=None):
         J, T = self.pr.n_jobs, self.pr.n_types
         dec = np.zeros(J, np.int64)

@@ -200,6 +200,79 @@ PlanOut plan_cost(const oracle_problem *pr, const Cell &cell, const std::vector<
   return {feasible, narrow(t_iter)};
 }
 
+// ---- NEXT-1: per-stage parallelism assembly ------
+// Each stage independently takes a DP x TP factorisation of its g = G/S GPUs:
+// mode 1 = the paper's assembled set, every stage DP-only or TP-only (2^S
+// plans); mode 2 = every factorisation per stage.  A stage's costs
+// are the §N5 terms evaluated with its own tp, dp and mb = GB/(B dp).
+struct StageCost {
+  bool ok;
+  i128 T, Tc, sync;  // Tc = the stage's inbound communication
+};
+
+std::vector<int32_t> stage_choices(int32_t mode, int32_t g) {
+  const int32_t K = ilog2(g);
+  std::vector<int32_t> ks;
+  if (mode == 1) {
+    ks.push_back(0);              // data-parallelism-only
+    if (K > 0) ks.push_back(K);   // tensor-parallelism-only
+  } else {
+    for (int32_t k = 0; k <= K; ++k) ks.push_back(k);
+  }
+  return ks;
+}
+
+StageCost stage_cost(const oracle_problem *pr, int32_t j, int32_t t, int32_t g, int32_t B,
+                     const std::vector<int32_t> &b, int32_t s, int32_t k) {
+  const int64_t off = pr->layer_off[j];
+  const int64_t TL = pr->layer_off[pr->n_jobs];
+  const i128 tp = (i128)1 << k, dp = (i128)g / tp, GB = pr->gb[j];
+  if (B * dp > GB) return {false, 0, 0, 0};
+  const i128 mb = GB / (B * dp);
+  const int64_t gpn = pr->gpn[t];
+  const int32_t *ck = pr->c + ((int64_t)t * (pr->k_max + 1) + k) * TL + off;
+  const bool tp_in = tp <= gpn, dp_in = (i128)g <= gpn;
+  const i128 a_tp = tp_in ? pr->alpha_in[t] : pr->alpha_x[t];
+  const i128 b_tp = tp_in ? pr->beta_in[t] : pr->beta_x[t];
+  const i128 a_dp = dp_in ? pr->alpha_in[t] : pr->alpha_x[t];
+  const i128 b_dp = dp_in ? pr->beta_in[t] : pr->beta_x[t];
+  i128 C = 0, TPV = 0, TPN = 0, W = 0, A = 0;
+  for (int32_t l = b[s]; l < b[s + 1]; ++l) {
+    C += ck[l];
+    TPV += pr->tpv[off + l];
+    TPN += pr->tpn[off + l];
+    W += pr->w[off + l];
+    A += pr->act[off + l];
+  }
+  const i128 mem = cdiv((i128)pr->kst[j] * W + (GB / dp) * A, tp);
+  if (mem > pr->mem[t]) return {false, 0, 0, 0};
+  i128 inb = 0;
+  if (s > 0) {
+    const bool b_in = ((i128)g < gpn) && ((int64_t)s % (gpn / (int64_t)g) != 0);
+    const i128 a_b = b_in ? pr->alpha_in[t] : pr->alpha_x[t];
+    const i128 b_b = b_in ? pr->beta_in[t] : pr->beta_x[t];
+    const i128 V = mb * pr->bnd[off + b[s] - 1];
+    inb = P2P(a_b, b_b, cdiv(V, tp)) + AG(tp, a_tp, b_tp, V);
+  }
+  const i128 T = mb * C + AR(tp, a_tp, b_tp, mb * TPV, TPN) + inb;
+  return {true, T, inb, AR(dp, a_dp, b_dp, cdiv(W, tp), 1)};
+}
+
+// Pipeline latency of one assembled plan: sum_s T_s + (B-1) * (T_s* - [form 1] Tc_s*)
+// + max_s sync_s, s* = the first slowest stage (north_star form 0; paper form 1).
+i128 assembled_latency(const std::vector<StageCost> &st, int32_t B, int32_t form) {
+  i128 sum = 0, mx = -1, tc = 0, sy = 0;
+  for (const StageCost &c : st) {
+    sum += c.T;
+    if (c.T > mx) {
+      mx = c.T;
+      tc = c.Tc;
+    }
+    sy = std::max(sy, c.sync);
+  }
+  return sum + (i128)(B - 1) * (mx - (form == 1 ? tc : 0)) + sy;
+}
+
 bool valid_problem(const oracle_problem *pr) {
   if (!pr || pr->n_types < 1 || pr->n_jobs < 0 || pr->k_max < 0) return false;
   if (pr->s_max < 1 || pr->g_max < 1 || pr->g_max > (1 << pr->k_max) || pr->depth < 0) return false;
@@ -297,6 +370,89 @@ int oracle_estimate(const oracle_problem *pr, const int32_t *cell_job, const int
       t_ns[i - c0] = best;
       plan[i - c0] = best_p;
     }
+  } catch (Overflow &) {
+    return 7;
+  }
+  return 0;
+}
+
+// NEXT-1 estimate: for Cells [c0, c1), every microbatch count and every
+// assembled plan (brute force over the product of the per-stage choices).
+// t_ns = best latency, bidx = its B index (lowest on ties), stage_k[(i-c0)*kstride + s]
+// = log2 tp of stage s in the first best plan found (-1 padding).
+int oracle_estimate_assembled(const oracle_problem *pr, int32_t mode, int32_t form,
+                              const int32_t *cell_job, const int32_t *cell_type,
+                              const int32_t *cell_G, const int32_t *cell_S, int64_t c0,
+                              int64_t c1, int64_t *t_ns, int32_t *bidx, int8_t *stage_k,
+                              int32_t kstride) {
+  if (!valid_problem(pr) || c0 < 0 || c1 < c0 || (mode != 1 && mode != 2) ||
+      (form != 0 && form != 1))
+    return 2;
+  try {
+    for (int64_t i = c0; i < c1; ++i) {
+      const int32_t j = cell_job[i], t = cell_type[i], G = cell_G[i], S = cell_S[i];
+      if (S > kstride) return 2;
+      const int32_t g = G / S;
+      const std::vector<int32_t> b = split(pr, j, t, S);
+      const std::vector<int32_t> ks = stage_choices(mode, g);
+      i128 best = -1;
+      int32_t best_b = -1;
+      std::vector<int32_t> best_k(S, -1);
+      for (int32_t bi = 0; bi < n_bvalues(pr); ++bi) {
+        const int32_t B = b_value(pr, S, bi);
+        // per-stage cost of every choice
+        std::vector<std::vector<StageCost>> tab(S, std::vector<StageCost>(ks.size()));
+        for (int32_t s = 0; s < S; ++s)
+          for (size_t q = 0; q < ks.size(); ++q) tab[s][q] = stage_cost(pr, j, t, g, B, b, s, ks[q]);
+        std::vector<size_t> digit(S, 0);  // mixed-radix counter, stage 0 least significant
+        for (;;) {
+          bool ok = true;
+          std::vector<StageCost> st(S);
+          for (int32_t s = 0; s < S; ++s) {
+            st[s] = tab[s][digit[s]];
+            ok = ok && st[s].ok;
+          }
+          if (ok) {
+            const i128 F = assembled_latency(st, B, form);
+            if (best < 0 || F < best) {
+              best = F;
+              best_b = bi;
+              for (int32_t s = 0; s < S; ++s) best_k[s] = ks[digit[s]];
+            }
+          }
+          int32_t s = 0;
+          while (s < S && ++digit[s] == ks.size()) digit[s++] = 0;
+          if (s == S) break;
+        }
+      }
+      t_ns[i - c0] = best < 0 ? INF : narrow(best);
+      bidx[i - c0] = best_b;
+      for (int32_t s = 0; s < kstride; ++s)
+        stage_k[(i - c0) * kstride + s] = (int8_t)(s < S ? best_k[s] : -1);
+    }
+  } catch (Overflow &) {
+    return 7;
+  }
+  return 0;
+}
+
+// NEXT-1: latency of one given assembled plan (stage_k[s] = log2 tp of stage s).
+int oracle_assembled_cost(const oracle_problem *pr, int32_t form, int32_t j, int32_t t, int32_t G,
+                          int32_t S, int32_t bi, const int8_t *stage_k, int64_t *latency,
+                          int32_t *feasible) {
+  if (!valid_problem(pr) || S < 1 || G % S || bi < 0 || bi >= n_bvalues(pr)) return 2;
+  try {
+    const int32_t g = G / S, B = b_value(pr, S, bi);
+    const std::vector<int32_t> b = split(pr, j, t, S);
+    std::vector<StageCost> st(S);
+    bool ok = true;
+    for (int32_t s = 0; s < S; ++s) {
+      if (stage_k[s] < 0 || (1 << stage_k[s]) > g) return 2;
+      st[s] = stage_cost(pr, j, t, g, B, b, s, stage_k[s]);
+      ok = ok && st[s].ok;
+    }
+    *feasible = ok ? 1 : 0;
+    *latency = ok ? narrow(assembled_latency(st, B, form)) : INF;
   } catch (Overflow &) {
     return 7;
   }

@@ -58,6 +58,20 @@ int oracle_estimate(const oracle_problem *pr, const int32_t *cell_job, const int
                     const int32_t *cell_G, const int32_t *cell_S, const int32_t *cell_nplans,
                     int64_t c0, int64_t c1, int64_t *t_ns, int32_t *plan);
 
+/* NEXT-1: per-stage parallelism assembly.  mode 1 = each
+ * stage DP-only or TP-only (the paper's 2^S assembled plans),
+ * mode 2 = every DP x TP factorisation per stage; form 0 = sum + (B-1) max,
+ * form 1 = sum + (B-1)(T_s* - T_comm,s*).  Brute force over
+ * every assembled plan and microbatch count.  stage_k: [c1-c0][kstride]. */
+int oracle_estimate_assembled(const oracle_problem *pr, int32_t mode, int32_t form,
+                              const int32_t *cell_job, const int32_t *cell_type,
+                              const int32_t *cell_G, const int32_t *cell_S, int64_t c0,
+                              int64_t c1, int64_t *t_ns, int32_t *bidx, int8_t *stage_k,
+                              int32_t kstride);
+int oracle_assembled_cost(const oracle_problem *pr, int32_t form, int32_t j, int32_t t, int32_t G,
+                          int32_t S, int32_t bi, const int8_t *stage_k, int64_t *latency,
+                          int32_t *feasible);
+
 /* O5: the §N6 round over all Cells.  free_in may be NULL (= capacity).
  * decision[j] = Cell id | -1 pending | -2 unschedulable. */
 int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,

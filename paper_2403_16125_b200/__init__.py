@@ -58,6 +58,10 @@ class _Config(C.Structure):
                 ("search_depth", C.c_int32)]
 
 
+class _Assembly(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("pipeline_form", C.c_int32)]
+
+
 class _CellView(C.Structure):
     _fields_ = [("n_cells", C.c_int64), ("n_cell_plans", C.c_int64), ("n_units", C.c_int64),
                 ("job", C.c_void_p), ("type", C.c_void_p), ("G", C.c_void_p), ("S", C.c_void_p),
@@ -66,7 +70,8 @@ class _CellView(C.Structure):
 
 
 EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_enumerate_cells", "crius_cells",
-           "crius_split_stride", "crius_partition_units", "crius_estimate_cells",
+           "crius_split_stride", "crius_max_stages", "crius_partition_units",
+           "crius_estimate_cells", "crius_estimate_assembled",
            "crius_compact_gathered", "crius_schedule_round", "crius_round_stats",
            "crius_kernel_launches",
            "crius_last_error", "crius_destroy"]
@@ -92,6 +97,9 @@ def lib():
         L.crius_split_stride.restype = i32
         L.crius_partition_units.argtypes = [vp, i32, vp, vp, vp]
         L.crius_estimate_cells.argtypes = [vp, i64, i64, vp, vp, vp]
+        L.crius_estimate_assembled.argtypes = [vp, C.POINTER(_Assembly), i64, i64, vp, vp, vp]
+        L.crius_max_stages.argtypes = [vp]
+        L.crius_max_stages.restype = i32
         L.crius_compact_gathered.argtypes = [vp, vp, i64, i32, vp, vp, vp]
         L.crius_schedule_round.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.crius_round_stats.argtypes = [vp, vp, vp]
@@ -228,6 +236,27 @@ class Crius:
         sp = C.c_void_p(splits.data_ptr()) if splits is not None else None
         _check(lib().crius_estimate_cells(self.ctx, int(unit_begin), int(unit_end),
                                           C.c_void_p(out.data_ptr()), sp, _stream_handle(stream)))
+        return out
+
+    def max_stages(self):
+        return lib().crius_max_stages(self.ctx)
+
+    def estimate_assembled(self, mode=1, form=1, unit_begin=0, unit_end=None, out=None,
+                           stage_tp=None, stream=None):
+        """NEXT-1 per-stage assembly (mode 1: DP-only/TP-only per stage, the
+        paper's 2^S plans; mode 2: every factorisation per stage; form 1: the
+        paper's (B-1)(T_s* - T_comm) steady state).  Records as estimate();
+        stage_tp: optional int8 [n_cells, max_stages] device tensor."""
+        if self.n_cells is None:
+            self.enumerate(stream)
+        unit_end = self.n_units if unit_end is None else unit_end
+        if out is None:
+            out = self.new_results(self.n_cells)
+        cfg = _Assembly(mode, form)
+        sp = C.c_void_p(stage_tp.data_ptr()) if stage_tp is not None else None
+        _check(lib().crius_estimate_assembled(self.ctx, C.byref(cfg), int(unit_begin),
+                                              int(unit_end), C.c_void_p(out.data_ptr()), sp,
+                                              _stream_handle(stream)))
         return out
 
     def compact(self, gathered, chunk_stride, world, cell_begin, out=None, stream=None):

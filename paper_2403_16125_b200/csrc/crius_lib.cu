@@ -503,6 +503,8 @@ crius_status crius_cells(crius_ctx *c, crius_cell_view *v) {
   return CRIUS_OK;
 }
 
+int32_t crius_max_stages(const crius_ctx *c) { return c ? std::max(1, c->stat_smax) : 0; }
+
 int32_t crius_split_stride(const crius_ctx *c) {
   if (!c) return 0;
   int nsi = 0;
@@ -562,16 +564,21 @@ crius_status crius_partition_units(crius_ctx *c, int32_t world, int64_t *unit_be
   return CRIUS_OK;
 }
 
-crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit_end,
-                                  crius_cell_result *d_out, int16_t *d_splits, void *stream) {
-  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+}  // extern "C"
+
+namespace {
+
+// Shared launcher of k_estimate: amode 0 = uniform plans (§N5), 1/2 = NEXT-1
+// per-stage assembly (paper DP-only/TP-only per stage; every factorisation).
+crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_begin,
+                             int64_t unit_end, crius_cell_result *d_out, int16_t *d_splits,
+                             int8_t *d_stage_tp, cudaStream_t st) {
   if (!c->enumerated) return fail(CRIUS_ESTATE, "estimate before enumerate");
   if (unit_begin < 0 || unit_end > c->n_units || unit_begin > unit_end)
     return fail(CRIUS_EINVAL, "bad unit range");
   if (!d_out) return fail(CRIUS_EINVAL, "null d_out");
   if (unit_begin == unit_end) return CRIUS_OK;
   CK(cudaSetDevice(c->device));
-  cudaStream_t st = (cudaStream_t)stream;
   EstArgs A{};
   A.cG = c->C.G;
   A.cS = c->C.S;
@@ -584,6 +591,9 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   A.splits = d_splits;
   A.split_stride = crius_split_stride(c);
   A.work_counter = c->d_counter;
+  A.form = form;
+  A.stage_tp = d_stage_tp;
+  A.stage_stride = std::max(1, c->stat_smax);
   // per-warp shared-memory layout
   const int Lp = c->Lmax + 1;
   const int K1e = ilog2_host(std::max(1, c->stat_gmax)) + 1;
@@ -613,6 +623,8 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   A.off_NRAW = take(Lp * 4);
   A.off_POFF = take(maxCells * 8);
   A.off_ORD = take((maxCells + 1) * 4);
+  A.st_cap = amode ? Stop * (amode == 1 ? 2 : K1e) : 0;
+  A.off_ST = take(A.st_cap * 25);
   A.warp_bytes = o;
   const int64_t nunits = unit_end - unit_begin;
   CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
@@ -620,14 +632,20 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   if (4 * A.warp_bytes > 200 * 1024) warps = 1;
   if (A.warp_bytes > 220 * 1024) return fail(CRIUS_EINVAL, "unit too large for shared memory");
   const size_t smem = (size_t)warps * A.warp_bytes;
-  // one lane per (Cell, k, group of microbatch counts): 1 B per lane (B = 4S)
-  // or up to 8 of the configured B values per lane
-  const bool wide = c->P.b_mode == 1;
 #ifndef CRIUS_NBG_WIDE
 #define CRIUS_NBG_WIDE 4  // microbatch counts per lane in b_mode 1 (measured best)
 #endif
-  auto kern = warps == 4 ? (wide ? k_estimate<4, CRIUS_NBG_WIDE> : k_estimate<4, 1>)
-                         : (wide ? k_estimate<1, CRIUS_NBG_WIDE> : k_estimate<1, 1>);
+  // one lane per (Cell, k, group of microbatch counts): 1 B per lane (B = 4S)
+  // or up to CRIUS_NBG_WIDE of the configured B values per lane
+  const bool wide = c->P.b_mode == 1;
+  void (*kern)(Params, EstArgs) = nullptr;
+  if (amode == 0)
+    kern = warps == 4 ? (wide ? k_estimate<4, CRIUS_NBG_WIDE, 0> : k_estimate<4, 1, 0>)
+                      : (wide ? k_estimate<1, CRIUS_NBG_WIDE, 0> : k_estimate<1, 1, 0>);
+  else if (amode == 1)
+    kern = warps == 4 ? k_estimate<4, 1, 1> : k_estimate<1, 1, 1>;
+  else
+    kern = warps == 4 ? k_estimate<4, 1, 2> : k_estimate<1, 1, 2>;
   int per_sm = 1;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
@@ -638,6 +656,28 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   CKL();
   c->launches += 1;
   return CRIUS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit_end,
+                                  crius_cell_result *d_out, int16_t *d_splits, void *stream) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  return launch_estimate(c, 0, 0, unit_begin, unit_end, d_out, d_splits, nullptr,
+                         (cudaStream_t)stream);
+}
+
+crius_status crius_estimate_assembled(crius_ctx *c, const crius_assembly *asm_cfg,
+                                      int64_t unit_begin, int64_t unit_end,
+                                      crius_cell_result *d_out, int8_t *d_stage_tp, void *stream) {
+  if (!c || !asm_cfg) return fail(CRIUS_EINVAL, "null argument");
+  if (asm_cfg->mode != 1 && asm_cfg->mode != 2) return fail(CRIUS_EINVAL, "assembly mode must be 1 or 2");
+  if (asm_cfg->pipeline_form != 0 && asm_cfg->pipeline_form != 1)
+    return fail(CRIUS_EINVAL, "pipeline_form must be 0 or 1");
+  return launch_estimate(c, asm_cfg->mode, asm_cfg->pipeline_form, unit_begin, unit_end, d_out,
+                         nullptr, d_stage_tp, (cudaStream_t)stream);
 }
 
 crius_status crius_compact_gathered(crius_ctx *c, const crius_cell_result *d_gathered,

@@ -36,6 +36,11 @@ struct EstArgs {
   int32_t off_PC, off_PW, off_PA, off_PV, off_PN, off_BND, off_F, off_ARG, off_BD, off_CELL;
   int32_t off_CRAW, off_NRAW, off_POFF, off_ORD;
   int32_t warp_bytes;
+  // NEXT-1 per-stage assembly (AMODE > 0): pipeline form, per-stage output
+  int32_t form;            // 0: sum + (B-1) max; 1: sum + (B-1)(T_s* - T_comm,s*)
+  int8_t *stage_tp;        // optional [cell][stage_stride] log2 tp of the best plan
+  int32_t stage_stride;
+  int32_t off_ST, st_cap;  // per-warp stage table (st_cap entries)
 };
 
 // Inclusive prefix of a profile row into dst[0..L] (dst[0] = 0).
@@ -243,6 +248,151 @@ __device__ __forceinline__ int64_t plan_group_time(const UnitCtx &U, int G, int 
   return best;
 }
 
+// ---- NEXT-1: per-stage parallelism assembly ------------------------------
+// Terms of stage s (layers [a, e)) run with tp = 2^k, dp = g/tp and mb =
+// GB/(B dp) (§N5 evaluated with the stage's own factorisation): T, its inbound
+// communication Tc (the term PAPER.md:382-384 overlaps), sync; false if the
+// stage does not fit (B dp > GB or memory).
+__device__ __forceinline__ bool stage_terms(const UnitCtx &U, int lg, int k, int lB, int s, int a,
+                                            int e, int64_t &T, int64_t &Tc, int64_t &sync) {
+  const int ldp = lg - k;
+  if (lB + ldp > U.lGB) return false;
+  const int lmb = U.lGB - lB - ldp;
+  const uint64_t tp = 1ull << k, dp = 1ull << ldp;
+  const bool tp_in = k <= U.lgpn, dp_in = lg <= U.lgpn;
+  const uint64_t a_tp = tp_in ? U.a_in : U.a_x, b_tp = tp_in ? U.b_in : U.b_x;
+  const uint64_t a_dp = dp_in ? U.a_in : U.a_x, b_dp = dp_in ? U.b_in : U.b_x;
+  const int64_t *PCk = U.PC + k * U.Lp;
+  const int64_t W = U.PW[e] - U.PW[a], A = U.PA[e] - U.PA[a];
+  const uint64_t mem = ((uint64_t)(U.kst * W + (A << (U.lGB - ldp))) + tp - 1) >> k;
+  if (mem > (uint64_t)U.memt) return false;
+  uint64_t t = (uint64_t)(PCk[e] - PCk[a]) << lmb;
+  if (k) {
+    const uint64_t V = (uint64_t)(U.PV[e] - U.PV[a]) << lmb;
+    t += (uint64_t)(U.PN[e] - U.PN[a]) * (2 * (tp - 1)) * a_tp + mul_shr_ceil(2 * (tp - 1) * V, b_tp, k + 20);
+  }
+  uint64_t inb = 0;
+  if (s) {
+    const int node_mask = lg < U.lgpn ? (1 << (U.lgpn - lg)) - 1 : 0;
+    const uint64_t Vb = (uint64_t)U.BND[a - 1] << lmb;
+    const bool b_in = (s & node_mask) != 0;
+    inb = (b_in ? U.a_in : U.a_x) + mul_shr_ceil((Vb + tp - 1) >> k, b_in ? U.b_in : U.b_x, 20);
+    if (k) inb += (tp - 1) * a_tp + mul_shr_ceil((tp - 1) * Vb, b_tp, k + 20);
+  }
+  T = (int64_t)(t + inb);
+  Tc = (int64_t)inb;
+  sync = 0;
+  if (ldp) {
+    const uint64_t Wt = ((uint64_t)W + tp - 1) >> k;
+    sync = (int64_t)(2 * (dp - 1) * a_dp + mul_shr_ceil(2 * (dp - 1) * Wt, b_dp, ldp + 20));
+  }
+  return true;
+}
+
+// Exact optimum over the assembled plans of one Cell (AMODE 1: each stage
+// DP-only or TP-only, the paper's 2^S plans; AMODE 2: every
+// factorisation per stage) without enumerating them.  Enumerate the slowest
+// stage s* with its choice (fixing M = T_s*, Tc_s*) and a bound Y on the max
+// sync; every other stage then independently takes its cheapest choice with
+// T < M (stages before s*: s* is the FIRST slowest) or T <= M (after), sync <= Y.
+// F(s*, q*, Y) = sum + (B-1)(M - [form] Tc*) + Y bounds the latency of that
+// plan from above and equals it for the optimum's own (s*, q*, max sync), so
+// the minimum over all enumerations is the optimum and the plan built at the
+// minimiser attains it.  Lanes split the (s*, q*) candidates.
+template <int AMODE>
+__device__ void assembled_cell(const UnitCtx &U, const EstArgs &A, int G, int S, int lane,
+                               int64_t *STT, int64_t *STC, int64_t *STY, uint8_t *STOK,
+                               int64_t &bestF, int &bestB, int8_t *kout) {
+  const int lS = ilog2_pow2(S), lg = ilog2_pow2(G) - lS;
+  const int nq = AMODE == 1 ? (lg ? 2 : 1) : lg + 1;
+  const int E = S * nq;
+  const int16_t *bd = U.BD + (S - 1) + lS;
+  bestF = kInf;
+  bestB = -1;
+  int bestE = -1;
+  int64_t bestY = 0;
+  const int nBv = U.b_mode == 0 ? 1 : U.nB;
+  for (int bi = 0; bi < nBv; ++bi) {
+    const int lB = U.b_mode == 0 ? lS + 2 : U.lBv[bi];
+    for (int e = lane; e < E; e += 32) {
+      const int s = e / nq, q = e - s * nq;
+      const int k = AMODE == 1 ? (q ? lg : 0) : q;
+      int64_t T = 0, Tc = 0, sy = 0;
+      const bool ok = stage_terms(U, lg, k, lB, s, bd[s], bd[s + 1], T, Tc, sy);
+      STT[e] = T;
+      STC[e] = Tc;
+      STY[e] = sy;
+      STOK[e] = ok;
+    }
+    __syncwarp();
+    const int64_t Bm1 = (1ll << lB) - 1;
+    int64_t myF = kInf, myY = 0;
+    int myE = -1;
+    for (int es = lane; es < E; es += 32) {
+      if (!STOK[es]) continue;
+      const int ss = es / nq;
+      const int64_t M = STT[es], tcs = A.form ? STC[es] : 0, sys = STY[es];
+      for (int yi = 0; yi <= E; ++yi) {
+        if (yi < E && !STOK[yi]) continue;
+        const int64_t Y = yi < E ? STY[yi] : 0;
+        if (Y < sys) continue;
+        int64_t sum = 0;
+        bool ok = true;
+        for (int s = 0; s < S && ok; ++s) {
+          if (s == ss) continue;
+          int64_t bt = kInf;
+          for (int q = 0; q < nq; ++q) {
+            const int ee = s * nq + q;
+            const int64_t T = STT[ee];
+            if (STOK[ee] && STY[ee] <= Y && (s < ss ? T < M : T <= M) && T < bt) bt = T;
+          }
+          ok = bt != kInf;
+          sum += bt;
+        }
+        if (!ok) continue;
+        const int64_t F = sum + M + Bm1 * (M - tcs) + Y;
+        if (F < myF) {
+          myF = F;
+          myE = es;
+          myY = Y;
+        }
+      }
+    }
+    // warp min of F (first lane on ties: any minimiser is a valid plan)
+    int64_t wF = myF;
+    for (int d = 16; d > 0; d >>= 1) wF = min(wF, __shfl_xor_sync(0xffffffffu, wF, d));
+    const unsigned who = __ballot_sync(0xffffffffu, myF == wF && myE >= 0);
+    if (wF < bestF && who) {
+      const int src = __ffs(who) - 1;
+      bestF = wF;
+      bestB = bi;
+      bestE = __shfl_sync(0xffffffffu, myE, src);
+      bestY = __shfl_sync(0xffffffffu, myY, src);
+      // rebuild the plan now: the stage table is this B's
+      if (kout && lane == 0) {
+        const int ss = bestE / nq;
+        const int64_t M = STT[bestE];
+        for (int s = 0; s < S; ++s) {
+          int bq = bestE - ss * nq;
+          if (s != ss) {
+            int64_t bt = kInf;
+            for (int q = 0; q < nq; ++q) {
+              const int ee = s * nq + q;
+              const int64_t T = STT[ee];
+              if (STOK[ee] && STY[ee] <= bestY && (s < ss ? T < M : T <= M) && T < bt) {
+                bt = T;
+                bq = q;
+              }
+            }
+          }
+          kout[s] = (int8_t)(AMODE == 1 ? (bq ? lg : 0) : bq);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ---- cp.async (LDGSTS) staging: global -> shared without registers ---------
 __device__ __forceinline__ void cp_async4(void *sdst, const void *gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
@@ -359,7 +509,7 @@ __device__ __forceinline__ UnitMeta load_meta(const Params &P, const EstArgs &A,
 #ifndef CRIUS_EST_MINB
 #define CRIUS_EST_MINB 4  // <= 128 registers: 4 CTAs (16 warps) per SM
 #endif
-template <int WARPS, int NBG>
+template <int WARPS, int NBG, int AMODE>
 __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params P, EstArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -379,6 +529,9 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
   int32_t *NRAW = (int32_t *)(base + A.off_NRAW);  // [Lp] raw tp_calls, then the int32 P0
   int64_t *POFF = (int64_t *)(base + A.off_POFF);  // [maxCells] raw plan offsets
   int32_t *ORD = (int32_t *)(base + A.off_ORD);    // [maxCells] processing order (S desc)
+  int64_t *STT = (int64_t *)(base + A.off_ST);     // [st_cap] stage table (AMODE > 0)
+  int64_t *STC = STT + A.st_cap, *STY = STC + A.st_cap;
+  uint8_t *STOK = (uint8_t *)(STY + A.st_cap);
   const int Lp = A.Lp;
   const int64_t out_cell_base = A.ucb[A.unit_begin];
 
@@ -501,6 +654,26 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
     U.b_x = P.ty[t].b_x;
     U.lBv = P.lB;
 
+    if (AMODE > 0) {  // NEXT-1: per-stage assembly, one Cell at a time
+      for (int ci = 0; ci < nc; ++ci) {
+        int64_t F;
+        int bb;
+        int8_t *kout = A.stage_tp ? A.stage_tp + (cb + ci - out_cell_base) * A.stage_stride : nullptr;
+        if (kout)
+          for (int q = lane; q < A.stage_stride; q += 32) kout[q] = -1;
+        __syncwarp();
+        assembled_cell<AMODE>(U, A, CG[ci], CS[ci], lane, STT, STC, STY, STOK, F, bb, kout);
+        if (lane == 0) {
+          CellResult res;
+          res.t_ns = F;
+          res.plan = F == kInf ? -1 : bb;
+          res.flags = F == kInf ? 0 : 1;
+          A.out[cb + ci - out_cell_base] = res;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     // processing order: Cells by S descending (stable) so a 32-lane chunk runs
     // stage loops of one length; item = (Cell, k, group of NBG microbatch counts)
     const int ngrp = P.b_mode == 0 ? 1 : (P.nB + NBG - 1) / NBG;
