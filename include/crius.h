@@ -182,6 +182,20 @@ crius_status crius_estimate_assembled(crius_ctx *ctx, const crius_assembly *asse
                                       int64_t unit_begin, int64_t unit_end,
                                       crius_cell_result *d_out, int8_t *d_stage_tp, void *stream);
 
+/* NEXT-3: Cell-guided parallelism tuning.  Each
+ * stage's parallelism in the estimated plan is its favour; the stage is tuned
+ * only within its half of the factorisation axis -- DP favour: dp-only ..
+ * half-hybrid (k <= ceil(log2 g / 2)), TP favour: half-hybrid .. tp-only
+ * (k >= floor(log2 g / 2)); half-hybrid = sqrt(g) replicas x sqrt(g) tensor
+ * shards (Fig. pruning); for odd log2 g both neighbouring
+ * factorisations belong to both halves (matches SPEC.md's g=8 and g=16 examples).  The best plan of the pruned product (every B of the set) is
+ * returned like crius_estimate_assembled.  d_favor (DEVICE int8, same layout as
+ * d_stage_tp): log2 tp of each stage of the estimated plan; a stage favours TP
+ * iff its entry is > 0.  Asynchronous. */
+crius_status crius_tune_assembled(crius_ctx *ctx, int32_t pipeline_form, int64_t unit_begin,
+                                  int64_t unit_end, const int8_t *d_favor,
+                                  crius_cell_result *d_out, int8_t *d_stage_tp, void *stream);
+
 /* Largest stage count S of the enumerated Cells (row length of d_stage_tp). */
 int32_t crius_max_stages(const crius_ctx *ctx);
 

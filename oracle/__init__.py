@@ -152,6 +152,20 @@ class Oracle:
                                                  C.byref(lat), C.byref(fe)), "assembled_cost")
         return lat.value, bool(fe.value)
 
+    def tune_assembled(self, cells, form, favor, c0=0, c1=None):
+        n = len(cells["job"])
+        c1 = n if c1 is None else c1
+        favor = np.ascontiguousarray(favor, np.int8)
+        kstride = favor.shape[1]
+        t_ns = np.zeros(c1 - c0, np.int64)
+        bidx = np.zeros(c1 - c0, np.int32)
+        sk = np.zeros((c1 - c0) * kstride, np.int8)
+        self._check(self.L.oracle_tune_assembled(
+            C.byref(self.s), form, *[_ptr(cells[k]) for k in ("job", "type", "G", "S")],
+            C.c_int64(c0), C.c_int64(c1), _ptr(favor), kstride, _ptr(t_ns), _ptr(bidx), _ptr(sk)),
+            "tune_assembled")
+        return t_ns, bidx, sk.reshape(c1 - c0, kstride)
+
     def round(self, cells, t_ns, free_in=None):
         J, T = self.pr.n_jobs, self.pr.n_types
         dec = np.zeros(J, np.int64)
@@ -164,6 +178,12 @@ class Oracle:
                                         _ptr(t_ns), None if fi is None else _ptr(fi), _ptr(dec),
                                         _ptr(fa), C.byref(tot)), "round")
         return dec, fa, tot.value
+
+
+def tune_choices(g, tp_favour):
+    ks = np.zeros(16, np.int32)
+    n = lib().oracle_tune_choices(g, int(tp_favour), _ptr(ks))
+    return [int(k) for k in ks[:n]]
 
 
 def comm(kind, p, alpha, beta, V, n=1):

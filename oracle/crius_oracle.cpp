@@ -436,6 +436,81 @@ int oracle_estimate_assembled(const oracle_problem *pr, int32_t mode, int32_t fo
   return 0;
 }
 
+// NEXT-3: the factorisations a stage keeps under its favour
+// (tp_favour = the estimated plan ran the stage tensor-parallel).  The axis
+// runs dp-only (k = 0) .. tp-only (k = K = log2 g); half-hybrid = sqrt(g) x
+// sqrt(g) (Fig. pruning); for odd K both neighbours of the half point
+// are kept on both sides.
+std::vector<int32_t> tuned_choices(int32_t g, bool tp_favour) {
+  const int32_t K = ilog2(g);
+  std::vector<int32_t> ks;
+  for (int32_t k = 0; k <= K; ++k) {
+    const bool dp_half = 2 * k <= K + 1;  // k <= ceil(K/2)
+    const bool tp_half = k >= K / 2;      // k >= floor(K/2)
+    if (tp_favour ? tp_half : dp_half) ks.push_back(k);
+  }
+  return ks;
+}
+
+int oracle_tune_choices(int32_t g, int32_t tp_favour, int32_t *ks) {
+  std::vector<int32_t> v = tuned_choices(g, tp_favour != 0);
+  for (size_t i = 0; i < v.size(); ++i) ks[i] = v[i];
+  return (int)v.size();
+}
+
+// NEXT-3: best plan over the product of the pruned per-stage sets (brute
+// force), every B of the set.  favor[(i-c0)*kstride + s] = log2 tp of stage s
+// in the estimated plan (> 0 = TP favour).
+int oracle_tune_assembled(const oracle_problem *pr, int32_t form, const int32_t *cell_job,
+                          const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                          int64_t c0, int64_t c1, const int8_t *favor, int32_t kstride,
+                          int64_t *t_ns, int32_t *bidx, int8_t *stage_k) {
+  if (!valid_problem(pr) || c0 < 0 || c1 < c0 || (form != 0 && form != 1)) return 2;
+  try {
+    for (int64_t i = c0; i < c1; ++i) {
+      const int32_t j = cell_job[i], t = cell_type[i], G = cell_G[i], S = cell_S[i];
+      if (S > kstride) return 2;
+      const int32_t g = G / S;
+      const std::vector<int32_t> b = split(pr, j, t, S);
+      std::vector<std::vector<int32_t>> ch(S);
+      for (int32_t s = 0; s < S; ++s) ch[s] = tuned_choices(g, favor[(i - c0) * kstride + s] > 0);
+      i128 best = -1;
+      int32_t best_b = -1;
+      std::vector<int32_t> best_k(S, -1);
+      for (int32_t bi = 0; bi < n_bvalues(pr); ++bi) {
+        const int32_t B = b_value(pr, S, bi);
+        std::vector<size_t> digit(S, 0);
+        for (;;) {
+          std::vector<StageCost> st(S);
+          bool ok = true;
+          for (int32_t s = 0; s < S; ++s) {
+            st[s] = stage_cost(pr, j, t, g, B, b, s, ch[s][digit[s]]);
+            ok = ok && st[s].ok;
+          }
+          if (ok) {
+            const i128 F = assembled_latency(st, B, form);
+            if (best < 0 || F < best) {
+              best = F;
+              best_b = bi;
+              for (int32_t s = 0; s < S; ++s) best_k[s] = ch[s][digit[s]];
+            }
+          }
+          int32_t s = 0;
+          while (s < S && ++digit[s] == ch[s].size()) digit[s++] = 0;
+          if (s == S) break;
+        }
+      }
+      t_ns[i - c0] = best < 0 ? INF : narrow(best);
+      bidx[i - c0] = best_b;
+      for (int32_t s = 0; s < kstride; ++s)
+        stage_k[(i - c0) * kstride + s] = (int8_t)(s < S ? best_k[s] : -1);
+    }
+  } catch (Overflow &) {
+    return 7;
+  }
+  return 0;
+}
+
 // NEXT-1: latency of one given assembled plan (stage_k[s] = log2 tp of stage s).
 int oracle_assembled_cost(const oracle_problem *pr, int32_t form, int32_t j, int32_t t, int32_t G,
                           int32_t S, int32_t bi, const int8_t *stage_k, int64_t *latency,

@@ -72,6 +72,16 @@ int oracle_assembled_cost(const oracle_problem *pr, int32_t form, int32_t j, int
                           int32_t S, int32_t bi, const int8_t *stage_k, int64_t *latency,
                           int32_t *feasible);
 
+/* NEXT-3: Cell-guided tuning.  Choices of a
+ * stage of g GPUs under its favour (ks[] receives them, returns the count), and
+ * the brute-force best plan over the pruned product given each Cell's favour
+ * row (log2 tp of the estimated plan per stage, > 0 = tensor-parallel favour). */
+int oracle_tune_choices(int32_t g, int32_t tp_favour, int32_t *ks);
+int oracle_tune_assembled(const oracle_problem *pr, int32_t form, const int32_t *cell_job,
+                          const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                          int64_t c0, int64_t c1, const int8_t *favor, int32_t kstride,
+                          int64_t *t_ns, int32_t *bidx, int8_t *stage_k);
+
 /* O5: the §N6 round over all Cells.  free_in may be NULL (= capacity).
  * decision[j] = Cell id | -1 pending | -2 unschedulable. */
 int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,

@@ -71,7 +71,7 @@ class _CellView(C.Structure):
 
 EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_enumerate_cells", "crius_cells",
            "crius_split_stride", "crius_max_stages", "crius_partition_units",
-           "crius_estimate_cells", "crius_estimate_assembled",
+           "crius_estimate_cells", "crius_estimate_assembled", "crius_tune_assembled",
            "crius_compact_gathered", "crius_schedule_round", "crius_round_stats",
            "crius_kernel_launches",
            "crius_last_error", "crius_destroy"]
@@ -98,6 +98,7 @@ def lib():
         L.crius_partition_units.argtypes = [vp, i32, vp, vp, vp]
         L.crius_estimate_cells.argtypes = [vp, i64, i64, vp, vp, vp]
         L.crius_estimate_assembled.argtypes = [vp, C.POINTER(_Assembly), i64, i64, vp, vp, vp]
+        L.crius_tune_assembled.argtypes = [vp, i32, i64, i64, vp, vp, vp, vp]
         L.crius_max_stages.argtypes = [vp]
         L.crius_max_stages.restype = i32
         L.crius_compact_gathered.argtypes = [vp, vp, i64, i32, vp, vp, vp]
@@ -257,6 +258,21 @@ class Crius:
         _check(lib().crius_estimate_assembled(self.ctx, C.byref(cfg), int(unit_begin),
                                               int(unit_end), C.c_void_p(out.data_ptr()), sp,
                                               _stream_handle(stream)))
+        return out
+
+    def tune_assembled(self, favor, form=1, unit_begin=0, unit_end=None, out=None, stage_tp=None,
+                       stream=None):
+        """NEXT-3 Cell-guided tuning: favor = int8 [n_cells, max_stages] device tensor
+        (log2 tp per stage of the estimated plan, e.g. estimate_assembled's stage_tp)."""
+        if self.n_cells is None:
+            self.enumerate(stream)
+        unit_end = self.n_units if unit_end is None else unit_end
+        if out is None:
+            out = self.new_results(self.n_cells)
+        sp = C.c_void_p(stage_tp.data_ptr()) if stage_tp is not None else None
+        _check(lib().crius_tune_assembled(self.ctx, form, int(unit_begin), int(unit_end),
+                                          C.c_void_p(favor.data_ptr()), C.c_void_p(out.data_ptr()),
+                                          sp, _stream_handle(stream)))
         return out
 
     def compact(self, gathered, chunk_stride, world, cell_begin, out=None, stream=None):

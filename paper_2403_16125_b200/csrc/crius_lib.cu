@@ -572,7 +572,7 @@ namespace {
 // per-stage assembly (paper DP-only/TP-only per stage; every factorisation).
 crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_begin,
                              int64_t unit_end, crius_cell_result *d_out, int16_t *d_splits,
-                             int8_t *d_stage_tp, cudaStream_t st) {
+                             int8_t *d_stage_tp, const int8_t *d_favor, cudaStream_t st) {
   if (!c->enumerated) return fail(CRIUS_ESTATE, "estimate before enumerate");
   if (unit_begin < 0 || unit_end > c->n_units || unit_begin > unit_end)
     return fail(CRIUS_EINVAL, "bad unit range");
@@ -593,6 +593,7 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   A.work_counter = c->d_counter;
   A.form = form;
   A.stage_tp = d_stage_tp;
+  A.favor = d_favor;
   A.stage_stride = std::max(1, c->stat_smax);
   // per-warp shared-memory layout
   const int Lp = c->Lmax + 1;
@@ -623,7 +624,7 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   A.off_NRAW = take(Lp * 4);
   A.off_POFF = take(maxCells * 8);
   A.off_ORD = take((maxCells + 1) * 4);
-  A.st_cap = amode ? Stop * (amode == 1 ? 2 : K1e) : 0;
+  A.st_cap = amode ? Stop * (amode == 1 ? 2 : K1e) : 0;  // modes 2, 3: every k
   A.off_ST = take(A.st_cap * 25);
   A.warp_bytes = o;
   const int64_t nunits = unit_end - unit_begin;
@@ -644,8 +645,10 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
                       : (wide ? k_estimate<1, CRIUS_NBG_WIDE, 0> : k_estimate<1, 1, 0>);
   else if (amode == 1)
     kern = warps == 4 ? k_estimate<4, 1, 1> : k_estimate<1, 1, 1>;
-  else
+  else if (amode == 2)
     kern = warps == 4 ? k_estimate<4, 1, 2> : k_estimate<1, 1, 2>;
+  else
+    kern = warps == 4 ? k_estimate<4, 1, 3> : k_estimate<1, 1, 3>;
   int per_sm = 1;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
@@ -665,7 +668,7 @@ extern "C" {
 crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit_end,
                                   crius_cell_result *d_out, int16_t *d_splits, void *stream) {
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
-  return launch_estimate(c, 0, 0, unit_begin, unit_end, d_out, d_splits, nullptr,
+  return launch_estimate(c, 0, 0, unit_begin, unit_end, d_out, d_splits, nullptr, nullptr,
                          (cudaStream_t)stream);
 }
 
@@ -677,7 +680,17 @@ crius_status crius_estimate_assembled(crius_ctx *c, const crius_assembly *asm_cf
   if (asm_cfg->pipeline_form != 0 && asm_cfg->pipeline_form != 1)
     return fail(CRIUS_EINVAL, "pipeline_form must be 0 or 1");
   return launch_estimate(c, asm_cfg->mode, asm_cfg->pipeline_form, unit_begin, unit_end, d_out,
-                         nullptr, d_stage_tp, (cudaStream_t)stream);
+                         nullptr, d_stage_tp, nullptr, (cudaStream_t)stream);
+}
+
+crius_status crius_tune_assembled(crius_ctx *c, int32_t pipeline_form, int64_t unit_begin,
+                                  int64_t unit_end, const int8_t *d_favor,
+                                  crius_cell_result *d_out, int8_t *d_stage_tp, void *stream) {
+  if (!c || !d_favor) return fail(CRIUS_EINVAL, "null argument");
+  if (pipeline_form != 0 && pipeline_form != 1)
+    return fail(CRIUS_EINVAL, "pipeline_form must be 0 or 1");
+  return launch_estimate(c, 3, pipeline_form, unit_begin, unit_end, d_out, nullptr, d_stage_tp,
+                         d_favor, (cudaStream_t)stream);
 }
 
 crius_status crius_compact_gathered(crius_ctx *c, const crius_cell_result *d_gathered,

@@ -39,6 +39,7 @@ struct EstArgs {
   // NEXT-1 per-stage assembly (AMODE > 0): pipeline form, per-stage output
   int32_t form;            // 0: sum + (B-1) max; 1: sum + (B-1)(T_s* - T_comm,s*)
   int8_t *stage_tp;        // optional [cell][stage_stride] log2 tp of the best plan
+  const int8_t *favor;     // AMODE 3 (tuner): [cell][stage_stride] log2 tp of the estimated plan
   int32_t stage_stride;
   int32_t off_ST, st_cap;  // per-warp stage table (st_cap entries)
 };
@@ -302,9 +303,12 @@ __device__ __forceinline__ bool stage_terms(const UnitCtx &U, int lg, int k, int
 template <int AMODE>
 __device__ void assembled_cell(const UnitCtx &U, const EstArgs &A, int G, int S, int lane,
                                int64_t *STT, int64_t *STC, int64_t *STY, uint8_t *STOK,
-                               int64_t &bestF, int &bestB, int8_t *kout) {
+                               int64_t &bestF, int &bestB, int8_t *kout, const int8_t *fav) {
   const int lS = ilog2_pow2(S), lg = ilog2_pow2(G) - lS;
   const int nq = AMODE == 1 ? (lg ? 2 : 1) : lg + 1;
+  // half-hybrid point (sqrt(g) x sqrt(g), Fig. pruning); for odd log2 g it
+  // falls between two factorisations and both neighbours belong to both halves
+  const int kdp_hi = (lg + 1) >> 1, ktp_lo = lg >> 1;
   const int E = S * nq;
   const int16_t *bd = U.BD + (S - 1) + lS;
   bestF = kInf;
@@ -318,7 +322,11 @@ __device__ void assembled_cell(const UnitCtx &U, const EstArgs &A, int G, int S,
       const int s = e / nq, q = e - s * nq;
       const int k = AMODE == 1 ? (q ? lg : 0) : q;
       int64_t T = 0, Tc = 0, sy = 0;
-      const bool ok = stage_terms(U, lg, k, lB, s, bd[s], bd[s + 1], T, Tc, sy);
+      bool ok = stage_terms(U, lg, k, lB, s, bd[s], bd[s + 1], T, Tc, sy);
+      if (AMODE == 3) {  // tuner: DP favour keeps k <= khalf, TP favour keeps k >= khalf
+        const bool tp_fav = fav[s] > 0;
+        ok = ok && (tp_fav ? k >= ktp_lo : k <= kdp_hi);
+      }
       STT[e] = T;
       STC[e] = Tc;
       STY[e] = sy;
@@ -662,7 +670,8 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
         if (kout)
           for (int q = lane; q < A.stage_stride; q += 32) kout[q] = -1;
         __syncwarp();
-        assembled_cell<AMODE>(U, A, CG[ci], CS[ci], lane, STT, STC, STY, STOK, F, bb, kout);
+        const int8_t *fav = A.favor ? A.favor + (cb + ci - out_cell_base) * A.stage_stride : nullptr;
+        assembled_cell<AMODE>(U, A, CG[ci], CS[ci], lane, STT, STC, STY, STOK, F, bb, kout, fav);
         if (lane == 0) {
           CellResult res;
           res.t_ns = F;

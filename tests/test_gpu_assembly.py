@@ -81,3 +81,55 @@ def test_cfg4_sampled_paper_assembly(pkg, oracle_mod):
     rng = np.random.default_rng(4)
     small = np.where(cells["S"] <= 8)[0]
     check(oracle_mod, pr, got, 1, 1, sample=rng.choice(small, 300, replace=False))
+
+
+# ---------------------------------------------------------------- NEXT-3 tuner
+def run_tune(pkg, pr, favor_np, form):
+    import torch
+    with pkg.Crius(pr) as cr:
+        n, _, _ = cr.enumerate()
+        ms = cr.max_stages()
+        fav = torch.from_numpy(np.ascontiguousarray(favor_np[:, :ms], np.int8)).cuda()
+        sk = torch.full((max(n, 1), ms), -9, dtype=torch.int8, device="cuda")
+        res = cr.tune_assembled(fav, form, stage_tp=sk)
+        t_ns, b, fl = pkg.decode(res)
+        return t_ns[:n], b[:n], fl[:n], sk.cpu().numpy()[:n]
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("form", [0, 1])
+def test_tuner_seeded_favours(pkg, oracle_mod, seed, form):
+    """Favours are a seeded input: the tuned optimum is unique -> bit-exact."""
+    pr = W.random_tiny(900 + seed, max_layers=8, n_types=2, n_jobs=3)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    ms = int(cells["S"].max())
+    rng = np.random.default_rng(seed)
+    favor = rng.integers(0, 2, size=(len(cells["G"]), ms)).astype(np.int8) * 3
+    t_g, b_g, f_g, k_g = run_tune(pkg, pr, favor, form)
+    t_o, _, _ = o.tune_assembled(cells, form, favor)
+    assert np.array_equal(t_g, t_o)
+    for i in range(len(t_o)):
+        if t_o[i] == INF:
+            assert b_g[i] == -1 and f_g[i] == 0
+            continue
+        j, t, G, S = (int(cells[k][i]) for k in ("job", "type", "G", "S"))
+        ch = [oracle_mod.tune_choices(G // S, favor[i][s] > 0) for s in range(S)]
+        assert all(k_g[i][s] in ch[s] for s in range(S))
+        lat, ok = o.assembled_cost(form, j, t, G, S, int(b_g[i]), k_g[i])
+        assert ok and lat == t_g[i]
+
+
+def test_tuner_after_estimate_cfg2(pkg, oracle_mod):
+    """Estimate (paper assembly) -> favours -> tune, all on the GPU: the tuned
+    plan lies in the pruned space of the estimate's plan, attains the oracle's
+    brute-force optimum of that space and never loses to the estimate."""
+    pr = W.make_config(2)
+    for form in (0, 1):
+        t_e, b_e, f_e, k_e = run(pkg, pr, 1, form)
+        t_t, b_t, f_t, k_t = run_tune(pkg, pr, k_e, form)
+        o = oracle_mod.Oracle(pr)
+        cells = o.enumerate()
+        t_o, _, _ = o.tune_assembled(cells, form, k_e)
+        assert np.array_equal(t_t, t_o)
+        assert np.all(t_t <= t_e)
