@@ -269,9 +269,13 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
   CK(cudaMemcpyAsync(c->d_scratch + J, &big, 4, cudaMemcpyHostToDevice, st));
   k_profile_stats<<<J, 64, 0, st>>>(c->P, c->d_scratch, c->d_scratch + J);
   CKL();
-  k_priority_rank<<<(J + 255) / 256, 256, 0, st>>>(c->d_submit, c->d_id, J, c->d_rank, c->d_pi);
+  CK(cudaMemsetAsync(c->d_rank, 0, (size_t)J * 4, st));
+  const unsigned tiles = (unsigned)((J + 255) / 256);
+  k_priority_count<<<dim3(tiles, tiles), 256, 0, st>>>(c->d_submit, c->d_id, J, c->d_rank);
   CKL();
-  c->launches += 2;
+  k_priority_scatter<<<tiles, 256, 0, st>>>(c->d_rank, J, c->d_pi);
+  CKL();
+  c->launches += 3;
   std::vector<int32_t> stats(J + 1);
   CK(cudaMemcpyAsync(stats.data(), c->d_scratch, (J + 1) * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

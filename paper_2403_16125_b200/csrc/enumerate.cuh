@@ -177,26 +177,28 @@ __global__ void k_unit_fill(Params P, Cells C, int64_t n_units) {
 }
 
 // Round priority pi (A-18): rank[j] = #{i : (submit_i, id_i) < (submit_j, id_j)};
-// pi[rank[j]] = j.  Tiled all-pairs count (ids are unique -> a permutation).
-__global__ void __launch_bounds__(256) k_priority_rank(const int64_t *submit, const int64_t *id,
-                                                       int32_t J, int32_t *rank, int32_t *pi) {
+// pi[rank[j]] = j (ids are unique -> a permutation).  2-D tiled all-pairs count:
+// block (x, y) compares the 256 jobs of tile x with the 256 jobs of tile y.
+__global__ void __launch_bounds__(256) k_priority_count(const int64_t *submit, const int64_t *id,
+                                                        int32_t J, int32_t *rank) {
   __shared__ int64_t ss[256], si[256];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t mys = j < J ? submit[j] : 0, myi = j < J ? id[j] : 0;
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  const int i0 = blockIdx.y * 256;
+  const int i = i0 + threadIdx.x;
+  ss[threadIdx.x] = i < J ? submit[i] : INT64_MAX;
+  si[threadIdx.x] = i < J ? id[i] : INT64_MAX;
+  __syncthreads();
+  if (j >= J) return;
+  const int64_t mys = submit[j], myi = id[j];
+  const int n = min(256, J - i0);
   int r = 0;
-  for (int b0 = 0; b0 < J; b0 += 256) {
-    const int i = b0 + threadIdx.x;
-    ss[threadIdx.x] = i < J ? submit[i] : INT64_MAX;
-    si[threadIdx.x] = i < J ? id[i] : INT64_MAX;
-    __syncthreads();
-    const int n = min(256, J - b0);
-    for (int q = 0; q < n; ++q) r += (ss[q] < mys) || (ss[q] == mys && si[q] < myi);
-    __syncthreads();
-  }
-  if (j < J) {
-    rank[j] = r;
-    pi[r] = j;
-  }
+  for (int q = 0; q < n; ++q) r += (ss[q] < mys) || (ss[q] == mys && si[q] < myi);
+  if (r) atomicAdd(&rank[j], r);
+}
+
+__global__ void k_priority_scatter(const int32_t *rank, int32_t J, int32_t *pi) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < J) pi[rank[j]] = j;
 }
 
 // Device-side profile validation: min over c (must be >= 1) and per-job max c
