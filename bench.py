@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--assembly", type=int, default=0,
                     help="NEXT-1: 1 = per-stage DP-only/TP-only (paper), 2 = every factorisation")
     ap.add_argument("--form", type=int, default=1, help="pipeline form for --assembly (1 = paper)")
+    ap.add_argument("--tune", action="store_true",
+                    help="NEXT-3: after --assembly 1, tune every Cell in its favoured halves")
     return ap.parse_args()
 
 
@@ -61,6 +63,7 @@ def workload_name(a):
     v = f"-{a.variant}" if a.variant else ""
     s = f"x{a.scale}" if a.scale != 1 else ""
     m = f"-assembly{a.assembly}form{a.form}" if getattr(a, "assembly", 0) else ""
+    m += "-tuned" if getattr(a, "tune", False) else ""
     return f"cfg{a.config}{v}{s}{m}"
 
 
@@ -262,6 +265,8 @@ def main():
     gathered = cr.new_results(world * plan.chunk) if world > 1 else None
     full = cr.new_results(n_cells) if world > 1 else None
     cells_h = {k: v.cpu().numpy() for k, v in cr.cells().items()}
+    stage_tp = (torch.empty((max(n_cells, 1), cr.max_stages()), dtype=torch.int8, device=dev)
+                if a.assembly else None)
     flush = not a.no_flush
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
 
@@ -275,7 +280,10 @@ def main():
             sharded.ShardPlan(cr, world)  # partition is part of the step (a tiny kernel + D2H)
         e1.record(stream)
         if a.assembly:
-            cr.estimate_assembled(a.assembly, a.form, int(ub[rank]), int(ub[rank + 1]), out=mine)
+            cr.estimate_assembled(a.assembly, a.form, int(ub[rank]), int(ub[rank + 1]), out=mine,
+                                  stage_tp=stage_tp)
+            if a.tune:
+                cr.tune_assembled(stage_tp, a.form, int(ub[rank]), int(ub[rank + 1]), out=mine)
         else:
             cr.estimate(int(ub[rank]), int(ub[rank + 1]), out=mine)
         e2.record(stream)

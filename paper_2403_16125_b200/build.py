@@ -26,6 +26,16 @@ def up_to_date():
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
+def build_debug(out=None):
+    """libcrius with the device-side invariant checks (-DCRIUS_DEBUG)."""
+    out = out or os.path.join(ROOT, "variants", "libcrius_debug.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [os.environ.get("NVCC", "nvcc")] + NVCC_FLAGS + ["-DCRIUS_DEBUG", "-o", out,
+                                                           os.path.join(CSRC, "crius_lib.cu")]
+    subprocess.check_call(cmd)
+    return out
+
+
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB

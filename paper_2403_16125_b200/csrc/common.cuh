@@ -8,6 +8,22 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side invariant checks, compiled in only with -DCRIUS_DEBUG (compute-
+// sanitizer is unavailable on the GPU pool): a violated bound traps the kernel.
+#ifdef CRIUS_DEBUG
+#define CRIUS_CHECK(cond)                                                        \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      printf("CRIUS_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);    \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define CRIUS_CHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace crius {
 
 constexpr int64_t kInf = INT64_MAX;

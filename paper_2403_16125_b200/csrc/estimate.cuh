@@ -306,6 +306,7 @@ __device__ void assembled_cell(const UnitCtx &U, const EstArgs &A, int G, int S,
                                int64_t &bestF, int &bestB, int8_t *kout, const int8_t *fav) {
   const int lS = ilog2_pow2(S), lg = ilog2_pow2(G) - lS;
   const int nq = AMODE == 1 ? (lg ? 2 : 1) : lg + 1;
+  CRIUS_CHECK(S * nq <= A.st_cap);
   // half-hybrid point (sqrt(g) x sqrt(g), Fig. pruning); for odd log2 g it
   // falls between two factorisations and both neighbours belong to both halves
   const int kdp_hi = (lg + 1) >> 1, ktp_lo = lg >> 1;
@@ -570,6 +571,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
     const int npu = (int)(m.pe - pb);
     const int L = m.L;
     const int64_t off = m.off;
+    CRIUS_CHECK(nc <= A.maxCells && L + 1 <= A.Lp);
     // compute planes needed: k <= log2(max g), max g <= min(largest G of the unit, g_max)
     const int cap = P.ty[t].cap;
     const int gtop = P.gpu_set == 1 ? cap : (2 * m.ng <= cap ? 2 * m.ng : (m.ng <= cap ? m.ng : m.ng / 2));
@@ -604,6 +606,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
     smax = warp_max_int(smax);
     gmax = warp_max_int(gmax);
     const int K1u = ilog2_pow2(gmax) + 1;  // <= K1s
+    CRIUS_CHECK(K1u <= K1s && smax <= A.Stop);
     for (int k = 0; k < K1u; ++k) warp_prefix32(PC + k * Lp, CRAW + k * Lp, L, lane);
     warp_prefix_inplace(PW, L, lane);
     warp_prefix_inplace(PA, L, lane);
@@ -630,6 +633,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
       int b = L;
       for (int s = S; s >= 2; --s) {
         b = ARG[s * Lp + b];
+        CRIUS_CHECK(b >= s - 1 && b < L);
         bd[s - 1] = (int16_t)b;
       }
       bd[0] = 0;
@@ -733,6 +737,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
         }
         r = lo;
         const int ci = ORD[r], local = f - CP[r];
+        CRIUS_CHECK(ci >= 0 && ci < nc && local >= 0 && local < CP[r + 1] - CP[r]);
         const int kk = NBG == 1 ? local : local / ngrp, gg = NBG == 1 ? 0 : local - kk * ngrp;
         if (NBG == 1) {  // one microbatch count per lane: the per-plan evaluation
           p = P.b_mode == 0 ? kk : kk * P.nB + gg;

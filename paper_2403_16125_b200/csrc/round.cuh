@@ -327,6 +327,7 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
   // stale same-type caches -> list -> one warp per job
   for (int a = tid; a < n_adm; a += kRoundThreads)
     if (A.bi_opt[a] == -2) list[atomicAdd(&sh.n_dirty, 1)] = a;
+  CRIUS_CHECK(n_adm <= R.J);
   __syncthreads();
   for (int k = wid; k < sh.n_dirty; k += kRoundWarps) refresh_victim_cache(R, A, list[k]);
   __syncthreads();
@@ -553,6 +554,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       tb = t1;
     }
     const int q = pos0 + wid, wq = q - W.w0;
+    CRIUS_CHECK(q >= R.J || (wq >= 0 && wq < W.wn));
     int kind = 0, opt = -1, need = 0;
     if (q < R.J && W.ref[wq] != kInf) {
       const int nopt = W.nopt[wq], ngj = W.ng[wq];
@@ -644,6 +646,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
           if (sh.res_kind[f] == 2) {
             ++n_scale;
             const int m = sh.res_m[f], t = x.t;
+            CRIUS_CHECK(m >= 0 && m <= sh.len[t] && sh.seq_ok[t]);
             for (int mm = 0; mm < m; ++mm) {
               const int a = sh.mv_a[t][mm];
               changed |= (1u << A.t[a]) | (1u << sh.mv_t[t][mm]);
@@ -657,10 +660,12 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
           int w = f;
           for (;;) {  // commit job w (admitted directly, or the first job's scale result)
             const int wq0 = pos0 + w - W.w0, o = sh.res_opt[w];
+            CRIUS_CHECK(wq0 >= 0 && wq0 < W.wn && o >= 0 && o < W.nopt[wq0]);
             const OptRec y = W.opt[(size_t)wq0 * R.maxopt + o];
             sh.fr[y.t] -= y.G;
             changed |= 1u << y.t;
             const int na = sh.n_adm;
+        CRIUS_CHECK(na < R.J);
             adm_set(A, R, na, pos0 + w, o, y.G, y.t, y.T, W.score[(size_t)wq0 * R.maxopt + o]);
             A.nopt[na] = W.nopt[wq0];
             sh.n_adm += 1;
