@@ -100,6 +100,17 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
   R.cur[pos] = -1;
 }
 
+// Option records are read-only inside K6: load them through the non-coherent
+// (L1-cached) path so repeated scans of the same admitted jobs hit L1.
+__device__ __forceinline__ OptRec ldg_opt(const OptRec *p) {
+  const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(p));
+  OptRec r;
+  r.T = v.x;
+  r.G = (int32_t)(v.y & 0xffffffff);
+  r.t = (int32_t)(v.y >> 32);
+  return r;
+}
+
 __device__ __forceinline__ bool kappa_less(const OptRec &a, const OptRec &b) {
   if (a.T != b.T) return a.T < b.T;
   if (a.G != b.G) return a.G < b.G;
@@ -246,10 +257,10 @@ __device__ __forceinline__ void refresh_victim_cache(const RoundBuf &R, const Ad
   Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0};
   int gmin = INT32_MAX;
   for (int i2 = lane; i2 < nv; i2 += 32) {
-    const OptRec o2 = R.opt[(int64_t)v * R.maxopt + i2];
+    const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
     gmin = min(gmin, o2.G);
     if (i2 == cv || o2.t != t || o2.G >= Gc) continue;
-    const double s2 = R.score[(int64_t)v * R.maxopt + i2];
+    const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
     Cand c{1, __ddiv_rn(sc - s2, (double)(Gc - o2.G)), a, i2, Gc - o2.G, 0, o2.G, o2.t, o2.T, s2};
     if (cand_less(c, best)) best = c;
   }
@@ -278,9 +289,9 @@ __device__ __forceinline__ void other_type_move(RoundShared &sh, const RoundBuf 
   const double sc = A.sc[a];
   Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0};
   for (int i2 = lane; i2 < nv; i2 += 32) {
-    const OptRec o2 = R.opt[(int64_t)v * R.maxopt + i2];
+    const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
     if (o2.t == t || o2.G > f2[o2.t]) continue;
-    const double s2 = R.score[(int64_t)v * R.maxopt + i2];
+    const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
     Cand c{1, sc - s2, a, i2, Gc, 1, o2.G, o2.t, o2.T, s2};  // key holds the loss here
     if (cand_less(c, best)) best = c;
   }
