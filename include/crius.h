@@ -218,6 +218,21 @@ crius_status crius_schedule_round(crius_ctx *ctx, const crius_cell_result *d_all
                                   const int32_t *free_gpus, int64_t *decision,
                                   int32_t *free_after, double *total_score, void *stream);
 
+/* NEXT-4: one round from a cluster state, for multi-event
+ * simulation (Alg. 1: SchedArrival P:436-445 and SchedDeparture = retry the
+ * pending jobs then extra scheduling).  run_cell (HOST int64
+ * [n_jobs] or NULL): Cell a job currently runs on (-1 = not running); running
+ * jobs start admitted on the option of that Cell's (type, G), may be moved as
+ * victims or reverse-scaled, never evicted.  active (HOST uint8 [n_jobs] or
+ * NULL = all): jobs that take part (arrived, not finished); inactive jobs get
+ * decision -3.  free_gpus = free counts with the running jobs' GPUs taken.
+ * Ties between victims go to the earlier job in (submit, id) order.
+ * crius_schedule_round(..) == this call with run_cell = active = NULL. */
+crius_status crius_schedule_round_state(crius_ctx *ctx, const crius_cell_result *d_all,
+                                        const int32_t *free_gpus, const int64_t *run_cell,
+                                        const uint8_t *active, int64_t *decision,
+                                        int32_t *free_after, double *total_score, void *stream);
+
 /* Counters of the last round (HOST out16[21]): [0] speculative Phase A batches,
  * [1] victim-sequence recomputations, [2] SM cycles in them, [3] SM cycles of
  * Phase A, [4] SM cycles of Phase B, [5] admitted jobs, [6] admissions through

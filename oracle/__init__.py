@@ -166,6 +166,20 @@ class Oracle:
             "tune_assembled")
         return t_ns, bidx, sk.reshape(c1 - c0, kstride)
 
+    def round_state(self, cells, t_ns, free_in, run_cell=None, active=None):
+        J, T = self.pr.n_jobs, self.pr.n_types
+        dec = np.zeros(J, np.int64)
+        fa = np.zeros(T, np.int32)
+        tot = C.c_double()
+        fi = np.ascontiguousarray(free_in, np.int32)
+        rc, rcp = _opt_ptr(run_cell, np.int64)
+        ac, acp = _opt_ptr(active, np.uint8)
+        t_ns = np.ascontiguousarray(t_ns, np.int64)
+        self._check(self.L.oracle_round_state(
+            C.byref(self.s), C.c_int64(len(t_ns)), *[_ptr(cells[k]) for k in ("job", "type", "G", "S")],
+            _ptr(t_ns), _ptr(fi), rcp, acp, _ptr(dec), _ptr(fa), C.byref(tot)), "round_state")
+        return dec, fa, tot.value
+
     def round(self, cells, t_ns, free_in=None):
         J, T = self.pr.n_jobs, self.pr.n_types
         dec = np.zeros(J, np.int64)
@@ -178,6 +192,13 @@ class Oracle:
                                         _ptr(t_ns), None if fi is None else _ptr(fi), _ptr(dec),
                                         _ptr(fa), C.byref(tot)), "round")
         return dec, fa, tot.value
+
+
+def _opt_ptr(a, dtype):
+    if a is None:
+        return None, None
+    a = np.ascontiguousarray(a, dtype)
+    return a, _ptr(a)
 
 
 def tune_choices(g, tp_favour):

@@ -539,6 +539,18 @@ int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_
                  const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
                  const int64_t *t_ns, const int32_t *free_in, int64_t *decision,
                  int32_t *free_after, double *total_score) {
+  return oracle_round_state(pr, n_cells, cell_job, cell_type, cell_G, cell_S, t_ns, free_in,
+                            nullptr, nullptr, decision, free_after, total_score);
+}
+
+// NEXT-4: the round from a cluster state -- running jobs (run_cell >= 0) start
+// admitted on the option of their Cell's (type, G); inactive jobs are skipped
+// (decision -3).  With run_cell = active = NULL this is oracle_round.
+int oracle_round_state(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,
+                       const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                       const int64_t *t_ns, const int32_t *free_in, const int64_t *run_cell,
+                       const uint8_t *active, int64_t *decision, int32_t *free_after,
+                       double *total_score) {
   if (!valid_problem(pr) || n_cells < 0) return 2;
   const int32_t J = pr->n_jobs, TT = pr->n_types, d = pr->depth;
 
@@ -589,6 +601,14 @@ int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_
   std::vector<int32_t> fr(TT);
   for (int32_t t = 0; t < TT; ++t) fr[t] = free_in ? free_in[t] : pr->cap[t];
   std::vector<int32_t> cur(J, -1);  // index into O[j]; -1 = not admitted
+  auto is_active = [&](int32_t j) { return active == nullptr || active[j] != 0; };
+  for (int32_t j = 0; j < J; ++j)
+    if (is_active(j) && run_cell && run_cell[j] >= 0) {
+      const int64_t rc = run_cell[j];
+      for (int32_t i = 0; i < (int32_t)O[j].size(); ++i)
+        if (O[j][i].t == cell_type[rc] && O[j][i].G == cell_G[rc]) cur[j] = i;
+      if (cur[j] < 0) return 2;  // a running Cell must be one of the job's options
+    }
 
   // ScaleResource(j) (A-17): at most d victim moves per option trial.
   struct Move {
@@ -665,7 +685,7 @@ int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_
 
   // Phase A: SchedArrival
   for (int32_t j : pi) {
-    if (ref[j] == INF) continue;  // unschedulable
+    if (ref[j] == INF || !is_active(j) || cur[j] >= 0) continue;  // unschedulable / not a candidate
     int32_t best = -1;
     for (int32_t i = 0; i < (int32_t)O[j].size(); ++i) {
       const Opt &o = O[j][i];
@@ -706,7 +726,7 @@ int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_
   for (int32_t j : pi)
     if (cur[j] >= 0) total = total + score(j, O[j][cur[j]]);
   for (int32_t j = 0; j < J; ++j)
-    decision[j] = ref[j] == INF ? -2 : (cur[j] < 0 ? -1 : O[j][cur[j]].cell);
+    decision[j] = !is_active(j) ? -3 : ref[j] == INF ? -2 : (cur[j] < 0 ? -1 : O[j][cur[j]].cell);
   for (int32_t t = 0; t < TT; ++t) free_after[t] = fr[t];
   *total_score = total;
   return 0;

@@ -89,6 +89,14 @@ int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_
                  const int64_t *t_ns, const int32_t *free_in, int64_t *decision,
                  int32_t *free_after, double *total_score);
 
+/* NEXT-4: the round from a cluster state (running jobs start admitted on
+ * the option of their Cell's (type, G); inactive jobs get decision -3). */
+int oracle_round_state(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,
+                       const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                       const int64_t *t_ns, const int32_t *free_in, const int64_t *run_cell,
+                       const uint8_t *active, int64_t *decision, int32_t *free_after,
+                       double *total_score);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,7 +72,8 @@ class _CellView(C.Structure):
 EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_enumerate_cells", "crius_cells",
            "crius_split_stride", "crius_max_stages", "crius_partition_units",
            "crius_estimate_cells", "crius_estimate_assembled", "crius_tune_assembled",
-           "crius_compact_gathered", "crius_schedule_round", "crius_round_stats",
+           "crius_compact_gathered", "crius_schedule_round", "crius_schedule_round_state",
+           "crius_round_stats",
            "crius_kernel_launches",
            "crius_last_error", "crius_destroy"]
 
@@ -103,6 +104,7 @@ def lib():
         L.crius_max_stages.restype = i32
         L.crius_compact_gathered.argtypes = [vp, vp, i64, i32, vp, vp, vp]
         L.crius_schedule_round.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.crius_schedule_round_state.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.crius_round_stats.argtypes = [vp, vp, vp]
         L.crius_kernel_launches.argtypes = [vp]
         L.crius_kernel_launches.restype = i64
@@ -292,6 +294,22 @@ class Crius:
         fr = None if free is None else self._arr(free, np.int32)
         _check(lib().crius_schedule_round(self.ctx, C.c_void_p(results.data_ptr()), fr, _ptr(dec),
                                           _ptr(fa), C.byref(tot), _stream_handle(stream)))
+        return dec, fa, tot.value
+
+    def schedule_round_state(self, results, free, run_cell=None, active=None, stream=None):
+        """NEXT-4: one round from a cluster state (running jobs keep/may move their
+        Cells; inactive jobs are skipped with decision -3)."""
+        J, T = self.pr.n_jobs, self.pr.n_types
+        dec = np.zeros(J, np.int64)
+        fa = np.zeros(T, np.int32)
+        tot = C.c_double()
+        fr = np.ascontiguousarray(free, np.int32)
+        rc = None if run_cell is None else np.ascontiguousarray(run_cell, np.int64)
+        ac = None if active is None else np.ascontiguousarray(active, np.uint8)
+        _check(lib().crius_schedule_round_state(
+            self.ctx, C.c_void_p(results.data_ptr()), _ptr(fr), None if rc is None else _ptr(rc),
+            None if ac is None else _ptr(ac), _ptr(dec), _ptr(fa), C.byref(tot),
+            _stream_handle(stream)))
         return dec, fa, tot.value
 
     def round_stats(self, stream=None):

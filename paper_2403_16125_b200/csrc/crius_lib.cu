@@ -87,6 +87,10 @@ struct crius_ctx {
   double *d_score = nullptr;
   int64_t *d_opt_cell = nullptr, *d_ref = nullptr, *d_decision = nullptr;
   int32_t *d_nopt = nullptr, *d_rng = nullptr, *d_cur = nullptr, *d_free = nullptr;
+  int32_t *d_run_opt = nullptr;
+  int8_t *d_cand = nullptr;
+  int64_t *d_run_cell = nullptr;
+  uint8_t *d_active = nullptr;
   double *d_total = nullptr;
   int64_t *d_round_stats = nullptr;
   int32_t *d_list = nullptr;
@@ -106,7 +110,8 @@ void free_all(crius_ctx *c) {
                   c->d_round_stats, c->d_score, c->adm_glob.T, c->adm_glob.bi_T,
                   c->adm_glob.sc, c->adm_glob.bi_key, c->adm_glob.bi_s, c->adm_glob.pos,
                   c->adm_glob.cur, c->adm_glob.G, c->adm_glob.t, c->adm_glob.nopt,
-                  c->adm_glob.bi_opt, c->adm_glob.bi_G2, c->adm_glob.gmin, c->d_list};
+                  c->adm_glob.bi_opt, c->adm_glob.bi_G2, c->adm_glob.gmin, c->d_list,
+                  c->d_run_opt, c->d_cand, c->d_run_cell, c->d_active};
   for (void *p : ptrs)
     if (p) cudaFree(p);
 }
@@ -723,6 +728,14 @@ crius_status crius_compact_gathered(crius_ctx *c, const crius_cell_result *d_gat
 crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
                                   const int32_t *free_gpus, int64_t *decision, int32_t *free_after,
                                   double *total_score, void *stream) {
+  return crius_schedule_round_state(c, d_all, free_gpus, nullptr, nullptr, decision, free_after,
+                                    total_score, stream);
+}
+
+crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d_all,
+                                        const int32_t *free_gpus, const int64_t *run_cell,
+                                        const uint8_t *active, int64_t *decision,
+                                        int32_t *free_after, double *total_score, void *stream) {
   if (!c || !d_all || !decision || !free_after || !total_score)
     return fail(CRIUS_EINVAL, "null argument");
   if (!c->enumerated) return fail(CRIUS_ESTATE, "round before enumerate");
@@ -742,6 +755,10 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
     CK(dalloc(&c->d_free, 16));
     CK(dalloc(&c->d_total, 1));
     CK(dalloc(&c->d_round_stats, 24));
+    CK(dalloc(&c->d_run_opt, J));
+    CK(dalloc(&c->d_cand, J));
+    CK(dalloc(&c->d_run_cell, J));
+    CK(dalloc(&c->d_active, J));
   }
   std::vector<int32_t> fr(T);
   for (int t = 0; t < T; ++t) {
@@ -749,6 +766,13 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
     if (fr[t] < 0) return fail(CRIUS_EINVAL, "free_gpus must be >= 0");
   }
   CK(cudaMemcpyAsync(c->d_free, fr.data(), T * 4, cudaMemcpyHostToDevice, st));
+  if (run_cell) {
+    for (int j = 0; j < J; ++j)
+      if (run_cell[j] < -1 || run_cell[j] >= c->n_cells)
+        return fail(CRIUS_EINVAL, "run_cell out of range");
+    CK(cudaMemcpyAsync(c->d_run_cell, run_cell, (size_t)J * 8, cudaMemcpyHostToDevice, st));
+  }
+  if (active) CK(cudaMemcpyAsync(c->d_active, active, (size_t)J, cudaMemcpyHostToDevice, st));
   RoundBuf R{};
   R.J = J;
   R.T = T;
@@ -768,19 +792,25 @@ crius_status crius_schedule_round(crius_ctx *c, const crius_cell_result *d_all,
   R.total = c->d_total;
   R.stats = c->d_round_stats;
   R.list = c->d_list;
+  R.run_cell = run_cell ? c->d_run_cell : nullptr;
+  R.active = active ? c->d_active : nullptr;
+  R.run_opt = c->d_run_opt;
+  R.cand = c->d_cand;
   k_round_options<<<(J + 127) / 128, 128, 0, st>>>(c->P, c->C.unit_cell_begin, c->C.type, c->C.G,
                                                    (const CellResult *)d_all, R);
   CKL();
   // each admitted job holds >= 1 GPU: at most min(J, sum of free GPUs) records
   int64_t max_adm = 0;
   for (int t = 0; t < T; ++t) max_adm += fr[t];
+  if (run_cell)
+    for (int j = 0; j < J; ++j) max_adm += run_cell[j] >= 0;
   max_adm = std::min<int64_t>(max_adm, J);
   cudaFuncAttributes fa{};
   CK(cudaFuncGetAttributes(&fa, k_round_greedy));
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   const size_t budget = (size_t)optin - fa.sharedSizeBytes - 1024;  // dynamic next to static
-  const size_t per_job = (size_t)c->maxopt * (sizeof(OptRec) + 8) + 16;
+  const size_t per_job = (size_t)c->maxopt * (sizeof(OptRec) + 8) + 24;
   int adm_in_smem = max_adm <= kAdmSmem;
   size_t adm_bytes = adm_in_smem ? (size_t)kAdmSmem * kAdmBytes : 0;
   if (adm_in_smem && (budget - adm_bytes) / per_job < 32) {

@@ -49,6 +49,11 @@ struct RoundBuf {
   double *total;
   int64_t *stats;        // [16] counters (see crius_round_stats)
   int32_t *list;         // [J] scratch list (used when admitted records live in global memory)
+  // NEXT-4 round state (NULL = every job active, none running)
+  const int64_t *run_cell;  // [J] by job: Cell the job runs on, or -1
+  const uint8_t *active;    // [J] by job: the job takes part in this round
+  int32_t *run_opt;         // [J] by position: option index of the running Cell, or -1
+  int8_t *cand;             // [J] by position: 1 = Phase A candidate (active, not running)
 };
 
 __device__ __forceinline__ double score_of(int64_t ref, int64_t T) {
@@ -98,6 +103,17 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
   R.ref[pos] = ref;
   R.ng[pos] = ngj;
   R.cur[pos] = -1;
+  // round state: a running job keeps the option of its Cell's (type, G)
+  const bool act = R.active ? R.active[j] != 0 : true;
+  int ro = -1;
+  if (act && R.run_cell && R.run_cell[j] >= 0) {
+    const int64_t rc = R.run_cell[j];
+    for (int i = 0; i < n; ++i)
+      if (o[i].t == cType[rc] && o[i].G == cG[rc]) ro = i;
+    CRIUS_CHECK(ro >= 0);
+  }
+  R.run_opt[pos] = ro;
+  R.cand[pos] = (int8_t)(act && ro < 0 && ref != kInf);
 }
 
 // Option records are read-only inside K6: load them through the non-coherent
@@ -138,6 +154,7 @@ struct AdmView {
 struct JobWin {
   int64_t *ref;
   int32_t *nopt, *ng;
+  int8_t *cand;
   OptRec *opt;
   double *score;
   int cap, w0, wn;
@@ -171,7 +188,7 @@ struct RoundShared {
   // per-(type, warp) best move of the current step, with the move's option data
   double r_key[kRT][kRoundWarps], r_s2[kRT][kRoundWarps];
   int64_t r_T2[kRT][kRoundWarps];
-  int32_t r_a[kRT][kRoundWarps], r_i[kRT][kRoundWarps];
+  int32_t r_a[kRT][kRoundWarps], r_i[kRT][kRoundWarps], r_p[kRT][kRoundWarps];
   int32_t r_freed[kRT][kRoundWarps], r_other[kRT][kRoundWarps];
   int32_t r_G2[kRT][kRoundWarps], r_t2[kRT][kRoundWarps];
 };
@@ -212,32 +229,34 @@ struct Cand {
   int a, i, freed, other, G2, t2;
   int64_t T2;
   double s2;
+  int p;  // the victim's priority position: ties go to the earlier job (§N6)
 };
 
 __device__ __forceinline__ bool cand_less(const Cand &x, const Cand &y) {
   if (!x.have) return false;
   if (!y.have) return true;
   if (x.key != y.key) return x.key < y.key;
-  if (x.a != y.a) return x.a < y.a;
+  if (x.p != y.p) return x.p < y.p;
   return x.i < y.i;
 }
 
 // Warp-wide argmin of Cands (one per lane) -> winning lane or -1.
 __device__ __forceinline__ int warp_cand_argmin(const Cand &c) {
-  return warp_lex_argmin(c.have, ord_double(c.key), ((uint32_t)c.a << 8) | (uint32_t)c.i);
+  return warp_lex_argmin(c.have, ord_double(c.key), ((uint32_t)c.p << 8) | (uint32_t)c.i);
 }
 
 // Per-(type, warp) best-move slot: written only by the winning lane of its warp.
 __device__ __forceinline__ bool slot_take(RoundShared &sh, int t, int w, const Cand &c) {
-  const int sa = sh.r_a[t][w];
+  const int sa = sh.r_a[t][w], sp = sh.r_p[t][w];
   if (!c.have) return false;
   if (sa >= 0) {
     const double sk = sh.r_key[t][w];
-    if (!(c.key < sk || (c.key == sk && (c.a < sa || (c.a == sa && c.i < sh.r_i[t][w])))))
+    if (!(c.key < sk || (c.key == sk && (c.p < sp || (c.p == sp && c.i < sh.r_i[t][w])))))
       return false;
   }
   sh.r_key[t][w] = c.key;
   sh.r_a[t][w] = c.a;
+  sh.r_p[t][w] = c.p;
   sh.r_i[t][w] = c.i;
   sh.r_freed[t][w] = c.freed;
   sh.r_other[t][w] = c.other;
@@ -254,14 +273,14 @@ __device__ __forceinline__ void refresh_victim_cache(const RoundBuf &R, const Ad
   const int lane = threadIdx.x & 31;
   const int v = A.pos[a], cv = A.cur[a], Gc = A.G[a], t = A.t[a], nv = A.nopt[a];
   const double sc = A.sc[a];
-  Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0};
+  Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0, v};
   int gmin = INT32_MAX;
   for (int i2 = lane; i2 < nv; i2 += 32) {
     const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
     gmin = min(gmin, o2.G);
     if (i2 == cv || o2.t != t || o2.G >= Gc) continue;
     const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
-    Cand c{1, __ddiv_rn(sc - s2, (double)(Gc - o2.G)), a, i2, Gc - o2.G, 0, o2.G, o2.t, o2.T, s2};
+    Cand c{1, __ddiv_rn(sc - s2, (double)(Gc - o2.G)), a, i2, Gc - o2.G, 0, o2.G, o2.t, o2.T, s2, v};
     if (cand_less(c, best)) best = c;
   }
   gmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)gmin);
@@ -287,12 +306,12 @@ __device__ __forceinline__ void other_type_move(RoundShared &sh, const RoundBuf 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int v = A.pos[a], Gc = A.G[a], t = A.t[a], nv = A.nopt[a];
   const double sc = A.sc[a];
-  Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0};
+  Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0, v};
   for (int i2 = lane; i2 < nv; i2 += 32) {
     const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
     if (o2.t == t || o2.G > f2[o2.t]) continue;
     const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
-    Cand c{1, sc - s2, a, i2, Gc, 1, o2.G, o2.t, o2.T, s2};  // key holds the loss here
+    Cand c{1, sc - s2, a, i2, Gc, 1, o2.G, o2.t, o2.T, s2, v};  // key holds the loss here
     if (cand_less(c, best)) best = c;
   }
   const int src = warp_cand_argmin(best);
@@ -354,7 +373,7 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
     __syncthreads();
     for (int a0 = 0; a0 < n_adm; a0 += kRoundThreads) {
       const int a = a0 + tid;
-      Cand mine{0, 0.0, 0, 0, 0, 0, 0, 0, 0, 0.0};
+      Cand mine{0, 0.0, 0, 0, 0, 0, 0, 0, 0, 0.0, 0};
       int myt = -1;
       if (a < n_adm) {
         myt = A.t[a];
@@ -365,14 +384,14 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
           const int bo = A.bi_opt[a];
           if (bo >= 0)
             mine = Cand{1, A.bi_key[a], a, bo, A.G[a] - A.bi_G2[a], 0, A.bi_G2[a], myt, A.bi_T[a],
-                        A.bi_s[a]};
+                        A.bi_s[a], A.pos[a]};
           if (A.gmin[a] <= sh.fmax_other[myt]) list[atomicAdd(&sh.n_list, 1)] = a;
         }
       }
       // (i) cached same-type moves: per type, the warp's winner offers itself
       for (int t = 0; t < TT; ++t) {
         const bool v = myt == t && mine.have;
-        const int src = warp_lex_argmin(v, ord_double(mine.key), ((uint32_t)a << 8) | (uint32_t)mine.i);
+        const int src = warp_lex_argmin(v, ord_double(mine.key), ((uint32_t)mine.p << 8) | (uint32_t)mine.i);
         if (lane == src) slot_take(sh, t, wid, mine);
         __syncwarp();
       }
@@ -394,8 +413,9 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
       const int t = wid;
       const bool in = lane < kRoundWarps;
       const int ra = in ? sh.r_a[t][lane] : -1;
+      const int rp = in ? sh.r_p[t][lane] : 0;
       const int src = warp_lex_argmin(ra >= 0, ord_double(in ? sh.r_key[t][lane] : 0.0),
-                                      ((uint32_t)ra << 8) | (uint32_t)(in ? sh.r_i[t][lane] : 0));
+                                      ((uint32_t)rp << 8) | (uint32_t)(in ? sh.r_i[t][lane] : 0));
       if (src < 0) {
         if (lane == 0) sh.active[t] = 0;
       } else {
@@ -489,6 +509,7 @@ __device__ void load_window(JobWin &W, const RoundBuf &R, int w0) {
     W.ref[i] = R.ref[w0 + i];
     W.nopt[i] = R.nopt[w0 + i];
     W.ng[i] = R.ng[w0 + i];
+    W.cand[i] = R.cand[w0 + i];
   }
   const int n = wn * R.maxopt;
   const longlong2 *so = reinterpret_cast<const longlong2 *>(R.opt + (int64_t)w0 * R.maxopt);
@@ -526,6 +547,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
   p += (size_t)win_cap * 4;
   W.ng = (int32_t *)p;
   p += (size_t)win_cap * 4;
+  W.cand = (int8_t *)p;
+  p += (size_t)win_cap * 8;
   AdmView A = Aglob;
   if (adm_in_smem) {
     A.T = (int64_t *)p;
@@ -554,6 +577,30 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
   __syncthreads();
   long long c_start = clock64(), c_seq = 0, n_batches = 0, n_seq = 0, n_scale = 0, n_bb = 0;
   load_window(W, R, 0);
+  // running jobs start admitted, in priority order (NEXT-4 round state)
+  if (R.run_cell) {
+    __shared__ int32_t wsum[kRoundWarps];
+    int base = 0;
+    for (int p0 = 0; p0 < R.J; p0 += kRoundThreads) {
+      const int pos = p0 + tid;
+      const int ro = pos < R.J ? R.run_opt[pos] : -1;
+      const unsigned b = __ballot_sync(0xffffffffu, ro >= 0);
+      if (lane == 0) wsum[wid] = __popc(b);
+      __syncthreads();
+      int before = base;
+      for (int w = 0; w < wid; ++w) before += wsum[w];
+      if (ro >= 0) {
+        const int a = before + __popc(b & ((1u << lane) - 1));
+        const OptRec x = R.opt[(int64_t)pos * R.maxopt + ro];
+        adm_set(A, R, a, pos, ro, x.G, x.t, x.T, R.score[(int64_t)pos * R.maxopt + ro]);
+        A.nopt[a] = R.nopt[pos];
+      }
+      for (int w = 0; w < kRoundWarps; ++w) base += wsum[w];
+      __syncthreads();
+    }
+    if (tid == 0) sh.n_adm = base;
+    __syncthreads();
+  }
 
   // ---- Phase A: SchedArrival in priority order
   long long tb = clock64();
@@ -567,7 +614,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
     const int q = pos0 + wid, wq = q - W.w0;
     CRIUS_CHECK(q >= R.J || (wq >= 0 && wq < W.wn));
     int kind = 0, opt = -1, need = 0;
-    if (q < R.J && W.ref[wq] != kInf) {
+    if (q < R.J && W.cand[wq]) {
       const int nopt = W.nopt[wq], ngj = W.ng[wq];
       const int best = warp_best_option(W.opt + (size_t)wq * R.maxopt, nopt,
                                         [&](int, const OptRec &x) {
@@ -719,14 +766,23 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
     }
   }
 
-  // ---- Phase B: up to d sweeps of reverse scaling over admitted jobs
+  // ---- Phase B: up to d sweeps of reverse scaling over admitted jobs, in
+  // priority order (running jobs were admitted first: sort by position)
   const long long c_phaseB = clock64();
   const int n_adm = sh.n_adm;
+  int32_t *ord = list;
+  for (int a = tid; a < n_adm; a += kRoundThreads) {
+    const int pa = A.pos[a];
+    int r = 0;
+    for (int b = 0; b < n_adm; ++b) r += A.pos[b] < pa;
+    ord[r] = a;
+  }
+  __syncthreads();
   for (int sweep = 0; sweep < R.depth; ++sweep) {
     if (tid == 0) sh.any_change = 0;
     __syncthreads();
     for (int a0 = 0; a0 < n_adm;) {
-      const int a = a0 + wid;
+      const int a = a0 + wid < n_adm ? ord[a0 + wid] : n_adm;
       int opt = -1;
       if (a < n_adm) {
         const int pos = A.pos[a], cv = A.cur[a], Gc = A.G[a], tc = A.t[a];
@@ -753,7 +809,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
         const unsigned fmask = __ballot_sync(0xffffffffu, lane < kRoundWarps && sh.res_opt[lane] >= 0);
         const int f = fmask ? __ffs(fmask) - 1 : kRoundWarps;
         if (tid == 0 && f < kRoundWarps) {
-          const int aa = a0 + f;
+          const int aa = ord[a0 + f];
           sh.fr[A.t[aa]] += A.G[aa];
           adm_set(A, R, aa, A.pos[aa], sh.res_opt[f], sh.res_G[f], sh.res_t[f], sh.res_T[f],
                   sh.res_sc[f]);
@@ -773,7 +829,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
   // ---- total score in priority order (fp64, sequential: bit-reproducible)
   if (tid == 0) {
     double tot = 0.0;
-    for (int a = 0; a < n_adm; ++a) tot = __dadd_rn(tot, A.sc[a]);
+    for (int k = 0; k < n_adm; ++k) tot = __dadd_rn(tot, A.sc[ord[k]]);
     *R.total = tot;
     if (R.stats) {
       R.stats[0] = n_batches;
@@ -794,7 +850,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
   for (int pos = tid; pos < R.J; pos += kRoundThreads) {
     const int j = R.pi[pos];
     const int c = R.cur[pos];
-    R.decision[j] = R.ref[pos] == kInf ? -2 : (c < 0 ? -1 : R.opt_cell[(int64_t)pos * R.maxopt + c]);
+    const bool act = R.active ? R.active[j] != 0 : true;
+    R.decision[j] = !act ? -3 : R.ref[pos] == kInf ? -2 : (c < 0 ? -1 : R.opt_cell[(int64_t)pos * R.maxopt + c]);
   }
 }
 

@@ -405,3 +405,39 @@ def test_sweep_best_never_worse_than_gpipe_rule(oracle_mod):
     ta, _ = a.estimate(ca)
     tb, _ = b.estimate(cb)
     assert np.array_equal(ca["G"], cb["G"]) and np.all(tb <= ta)
+
+
+# ---------------------------------------------------------------- NEXT-4 round state
+def test_round_state_hand_vector(oracle_mod):
+    fx = golden("round_state.json")
+    for d, key in ((1, "d1"), (3, "d1"), (0, "d0")):
+        pr, cells, t_ns = _round_problem(fx, d)
+        run = np.full(pr.n_jobs, -1, np.int64)
+        for j, rc in enumerate(fx["running"]):
+            if rc is not None:
+                run[j] = [i for i in range(len(t_ns)) if cells["job"][i] == j and
+                          (cells["type"][i], cells["G"][i]) == tuple(rc)][0]
+        dec, fa, tot = oracle_mod.Oracle(pr).round_state(cells, t_ns, fx["free"], run_cell=run)
+        e = fx["expect"][key]
+        for j, ch in enumerate(e["choice"]):
+            if ch is None:
+                assert dec[j] == -1
+            else:
+                assert (int(cells["type"][dec[j]]), int(cells["G"][dec[j]])) == tuple(ch)
+        assert list(fa) == e["free_after"] and tot == e["total"]
+
+
+def test_round_state_reduces_to_round(oracle_mod):
+    """No running job and every job active: the state round is the round;
+    inactive jobs get -3 and are invisible to the others."""
+    pr = W.make_config(3)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    t_ns, _ = o.estimate(cells)
+    d1, f1, t1 = o.round(cells, t_ns)
+    d2, f2, t2 = o.round_state(cells, t_ns, pr.cap)
+    assert np.array_equal(d1, d2) and np.array_equal(f1, f2) and t1 == t2
+    act = np.zeros(pr.n_jobs, np.uint8)
+    act[::2] = 1
+    d3, _, _ = o.round_state(cells, t_ns, pr.cap, active=act)
+    assert np.all(d3[1::2] == -3) and np.all(d3[::2] != -3)
