@@ -1,0 +1,77 @@
+"""Oracle trace simulator for NEXT-4 -- TEST INFRASTRUCTURE ONLY.
+
+A plain, literal event loop over the oracle's round (oracle_round_state),
+written independently of paper_2403_16125_b200/sim.py; the two share no code.
+Semantics (reading R-8), integer nanoseconds:
+  - first start on Cell c at time s: finish = s + N * T(c)      (N iterations)
+  - restart (Cell change) at time t: the segment's completed iterations
+    floor((t - s - pen_seg) / T(c_old)) are kept; finish = t + P + N' * T(c_new)
+  - at each event time: completions leave, arrivals join, one round runs
+    over pending + running jobs; -2 drops a job; leftover pending = starved.
+"""
+import numpy as np
+
+NS = 10 ** 9
+
+
+def simulate(o, cells, t_ns, iterations, penalty_s=30):
+    pr = o.pr
+    J = pr.n_jobs
+    submit = [int(x) * NS for x in pr.submit]
+    iters = [int(x) for x in iterations]
+    P = int(penalty_s) * NS
+    status = ["future"] * J
+    run = [-1] * J
+    left = list(iters)
+    seg = [(0, 0)] * J          # (segment start, segment penalty)
+    fin = [-1] * J
+    first = [-1] * J
+    restarts = [0] * J
+    rounds = 0
+    while True:
+        t_next = [fin[j] for j in range(J) if status[j] == "running"]
+        t_next += [submit[j] for j in range(J) if status[j] == "future"]
+        if not t_next:
+            break
+        t = min(t_next)
+        for j in range(J):
+            if status[j] == "running" and fin[j] <= t:
+                status[j] = "done"
+                run[j] = -1
+        for j in range(J):
+            if status[j] == "future" and submit[j] <= t:
+                status[j] = "pending"
+        active = np.array([s in ("pending", "running") for s in status], np.uint8)
+        free = [int(c) for c in pr.cap]
+        for j in range(J):
+            if status[j] == "running":
+                free[int(cells["type"][run[j]])] -= int(cells["G"][run[j]])
+        dec, _, _ = o.round_state(cells, t_ns, free, run_cell=np.array(run, np.int64),
+                                  active=active)
+        rounds += 1
+        for j in range(J):
+            if not active[j]:
+                continue
+            d = int(dec[j])
+            if d == -2:
+                status[j] = "dropped"
+            elif d >= 0 and status[j] == "pending":
+                status[j] = "running"
+                run[j] = d
+                seg[j] = (t, 0)
+                if first[j] < 0:
+                    first[j] = t
+                fin[j] = t + left[j] * int(t_ns[d])
+            elif d >= 0 and d != run[j]:
+                s0, p0 = seg[j]
+                ran = t - s0 - p0
+                done_it = ran // int(t_ns[run[j]]) if ran > 0 else 0
+                left[j] -= min(done_it, left[j])
+                run[j] = d
+                seg[j] = (t, P)
+                fin[j] = t + P + left[j] * int(t_ns[d])
+                restarts[j] += 1
+    state = np.array([{"done": 3, "dropped": 4, "pending": 5, "future": 0}[s] for s in status],
+                     np.int8)
+    return dict(first_start=np.array(first, np.int64), finish=np.array(fin, np.int64),
+                restarts=np.array(restarts, np.int32), state=state, rounds=rounds)

@@ -1,0 +1,119 @@
+"""NEXT-4: multi-event trace simulation around the round.
+
+Crius schedules on events: a job's arrival triggers
+SchedArrival, a completion triggers SchedDeparture -- retry the pending jobs,
+then extra scheduling of the released resources (Alg. 1).  Every
+scheduling decision here is one `crius_schedule_round_state` call on the GPU
+(running jobs keep their Cells unless downscaled/moved as victims or scaled up
+in Phase B); this module only keeps the event clock and job states.
+
+Event semantics (reading R-8), all integer nanoseconds:
+  * a job with N iterations started on Cell c at time s finishes at
+    s + penalty + N * T(c) (T = the Cell's estimated iteration time); the
+    penalty is paid on every restart (Cell change), not on the first start;
+  * at an event time t: completions (finish <= t) leave and free their GPUs,
+    arrivals (submit <= t) join the pending set, then ONE round runs over the
+    pending + running jobs;
+  * a restarted job keeps the iterations completed in its segment:
+    done = floor((t - s - penalty) / T(c_old)) (>= 0);
+  * decision -2 (no feasible Cell) drops the job; the run ends when nothing is
+    running and no arrival is left (jobs still pending then are "starved").
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+NS = 1_000_000_000
+FUTURE, PENDING, RUNNING, DONE, DROPPED, STARVED = range(6)
+
+
+@dataclass
+class SimResult:
+    first_start: np.ndarray   # int64 ns (-1 never started)
+    finish: np.ndarray        # int64 ns (-1 never finished)
+    restarts: np.ndarray      # int32
+    state: np.ndarray         # int8 final state
+    rounds: int
+    events: list              # (t, n_started, n_restarted, n_finished) per round
+
+    def summary(self, submit_ns):
+        done = self.state == DONE
+        jct = (self.finish[done] - submit_ns[done]) / NS
+        q = (self.first_start[done] - submit_ns[done]) / NS
+        return {"jobs_done": int(done.sum()), "dropped": int((self.state == DROPPED).sum()),
+                "starved": int((self.state == STARVED).sum()), "rounds": self.rounds,
+                "avg_jct_s": float(jct.mean()) if done.any() else None,
+                "avg_queue_s": float(q.mean()) if done.any() else None,
+                "makespan_s": float(self.finish[done].max() / NS) if done.any() else None,
+                "avg_restarts": float(self.restarts[done].mean()) if done.any() else None}
+
+
+def simulate(cr, pr, iterations, penalty_s=30, results=None):
+    """Replay the Problem's trace through GPU rounds; `cr` is a Crius context."""
+    J = pr.n_jobs
+    if cr.n_cells is None:
+        cr.enumerate()
+    if results is None:
+        results = cr.estimate()
+    cells = {k: v.cpu().numpy() for k, v in cr.cells().items() if k in ("type", "G")}
+    t_cell = results[:cr.n_cells, 0].cpu().numpy()
+    submit = np.asarray(pr.submit, np.int64) * NS
+    iters = np.asarray(iterations, np.int64)
+    pen = int(penalty_s) * NS
+    state = np.full(J, FUTURE, np.int8)
+    run = np.full(J, -1, np.int64)
+    remaining = iters.copy()
+    seg_start = np.zeros(J, np.int64)
+    seg_pen = np.zeros(J, np.int64)
+    finish = np.full(J, -1, np.int64)
+    first = np.full(J, -1, np.int64)
+    restarts = np.zeros(J, np.int32)
+    events = []
+    order = np.argsort(submit, kind="stable")
+    nxt = 0
+    t = 0
+    while True:
+        running = np.where(state == RUNNING)[0]
+        t_fin = finish[running].min() if running.size else None
+        t_arr = submit[order[nxt]] if nxt < J else None
+        if t_fin is None and t_arr is None:
+            break
+        t = min(x for x in (t_fin, t_arr) if x is not None)
+        ended = running[finish[running] <= t]
+        state[ended] = DONE
+        run[ended] = -1
+        while nxt < J and submit[order[nxt]] <= t:
+            state[order[nxt]] = PENDING
+            nxt += 1
+        active = ((state == PENDING) | (state == RUNNING)).astype(np.uint8)
+        used = np.zeros(pr.n_types, np.int64)
+        for j in np.where(state == RUNNING)[0]:
+            used[cells["type"][run[j]]] += cells["G"][run[j]]
+        free = (np.asarray(pr.cap, np.int64) - used).astype(np.int32)
+        dec, _, _ = cr.schedule_round_state(results, free, run_cell=run, active=active)
+        n_start = n_restart = 0
+        for j in np.where(active == 1)[0]:
+            d = int(dec[j])
+            if d == -2:
+                state[j] = DROPPED
+            elif d >= 0:
+                if state[j] == PENDING:
+                    state[j] = RUNNING
+                    run[j], seg_start[j], seg_pen[j] = d, t, 0
+                    if first[j] < 0:
+                        first[j] = t
+                    finish[j] = t + int(remaining[j]) * int(t_cell[d])
+                    n_start += 1
+                elif d != run[j]:
+                    ran = t - seg_start[j] - seg_pen[j]
+                    done_it = max(0, ran // int(t_cell[run[j]])) if ran > 0 else 0
+                    remaining[j] -= min(done_it, remaining[j])
+                    run[j], seg_start[j], seg_pen[j] = d, t, pen
+                    finish[j] = t + pen + int(remaining[j]) * int(t_cell[d])
+                    restarts[j] += 1
+                    n_restart += 1
+        events.append((int(t), n_start, n_restart, int(ended.size)))
+    state[state == PENDING] = STARVED
+    return SimResult(first, finish, restarts, state, len(events), events)

@@ -358,3 +358,26 @@ def random_tiny(seed, *, max_layers=8, n_types=2, n_jobs=3, b_mode=None, gpu_set
                    s_max=int(rng.choice([1, 2, 4, 8])), g_max=int(rng.choice([1, 2, 4, 8])),
                    b_mode=bm, b_values=bv, depth=int(rng.integers(0, 4)),
                    model_names=[f"rand{j}" for j in range(J)])
+
+
+def iterations_for(pr, seed=0, lo=100, hi=5000):
+    """Training length of every job (iterations), log-uniform in [lo, hi]
+    (SPEC.md workload module's reading of the paper's trace adaptation)."""
+    rng = np.random.default_rng(10_000 + seed)
+    return np.exp(rng.uniform(np.log(lo), np.log(hi), size=pr.n_jobs)).astype(np.int64)
+
+
+def subset(pr, n_jobs):
+    """The first n_jobs jobs of a Problem (same cluster, tables sliced)."""
+    import copy
+    q = copy.copy(pr)
+    L = int(pr.layer_off[n_jobs])
+    for k in ("job_id", "submit", "ng", "gb", "kst", "n_layers"):
+        setattr(q, k, getattr(pr, k)[:n_jobs].copy())
+    q.layer_off = pr.layer_off[:n_jobs + 1].copy()
+    for k in ("w", "act", "bnd", "tpv", "tpn"):
+        setattr(q, k, getattr(pr, k)[:L].copy())
+    q.c = np.ascontiguousarray(pr.c[:, :, :L])
+    q.model_names = pr.model_names[:n_jobs]
+    q.name = f"{pr.name}[:{n_jobs}]"
+    return q

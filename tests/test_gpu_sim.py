@@ -1,0 +1,41 @@
+"""NEXT-4: the product trace simulator (GPU rounds, paper_2403_16125_b200.sim)
+vs the oracle simulator: identical start/finish times, restarts and final
+states on generated traces."""
+import numpy as np
+import pytest
+
+from paper_2403_16125_b200 import workload as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
+    from paper_2403_16125_b200 import build
+    build.build()
+    import paper_2403_16125_b200 as p
+    return p
+
+
+@pytest.mark.parametrize("cfg,n,depth,pen", [(2, 8, 3, 30), (3, 150, 3, 30), (3, 150, 0, 30),
+                                             (3, 300, 1, 120)])
+def test_sim_matches_oracle(pkg, oracle_mod, cfg, n, depth, pen):
+    from oracle import sim as osim
+    from paper_2403_16125_b200 import sim
+    pr = W.subset(W.make_config(cfg), n)
+    pr.depth = depth
+    it = W.iterations_for(pr, seed=cfg)
+    with pkg.Crius(pr) as cr:
+        got = sim.simulate(cr, pr, it, penalty_s=pen)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    t_ns, _ = o.estimate(cells)
+    want = osim.simulate(o, cells, t_ns, it, pen)
+    assert got.rounds == want["rounds"]
+    assert np.array_equal(got.first_start, want["first_start"])
+    assert np.array_equal(got.finish, want["finish"])
+    assert np.array_equal(got.restarts, want["restarts"])
+    assert np.array_equal(got.state, want["state"])
