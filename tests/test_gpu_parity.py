@@ -255,3 +255,35 @@ def test_loader_rejects_overflow(crius):
     with pytest.raises(pkg.CriusError) as e:
         pkg.Crius(pr)
     assert e.value.code == 2 and "2^52" in str(e.value)
+
+
+def test_cfg5_x10_sampled_units(crius, oracle_mod):
+    """100k-job stress (414 M plans): the GPU estimates everything; the oracle
+    re-derives the Cell table and recomputes 60 sampled units one by one."""
+    import torch
+    pkg = crius
+    pr = W.make_config(5, scale=10)
+    with pkg.Crius(pr) as cr:
+        n, p, u = cr.enumerate()
+        res = cr.estimate()
+        t_g, p_g, _ = pkg.decode(res)
+        cg = {k: v.cpu().numpy() for k, v in cr.cells().items()}
+        dec, fa, tot = cr.schedule_round(res)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    for k in ("job", "type", "G", "S", "nplans"):
+        assert np.array_equal(cg[k], cells[k]), k
+    unit = cells["job"].astype(np.int64) * pr.n_types + cells["type"]
+    ucb = np.searchsorted(unit, np.arange(u + 1), side="left")
+    rng = np.random.default_rng(50)
+    for uu in rng.choice(u, 60, replace=False):
+        c0, c1 = int(ucb[uu]), int(ucb[uu + 1])
+        if c0 < c1:
+            t_o, p_o = o.estimate(cells, c0, c1)
+            assert np.array_equal(t_g[c0:c1], t_o) and np.array_equal(p_g[c0:c1], p_o)
+    # the round: every admitted job on one of its own feasible Cells, capacity respected
+    used = np.zeros(pr.n_types, np.int64)
+    for j in np.where(dec >= 0)[0]:
+        assert cells["job"][dec[j]] == j and t_g[dec[j]] < INF
+        used[cells["type"][dec[j]]] += cells["G"][dec[j]]
+    assert np.all(used + fa == pr.cap)
