@@ -78,28 +78,49 @@ def config_dict(a, pr, n_cells, n_plans, world, flush):
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region through NVML
+    (every 2 ms); falls back to nvidia-smi if NVML is unavailable."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index):
         self.index = index
         self.rows = []
         self.stop = threading.Event()
         self.t = threading.Thread(target=self.run, daemon=True)
+        self.nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[index]) if vis else index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+        except Exception:
+            self.nv = None
 
     def run(self):
+        nv = self.nv
         while not self.stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                if nv is not None:
+                    sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    names = [n for n, attr in self.REASONS if r & getattr(nv, attr, 0)]
+                    self.rows.append((float(sm), float(self.smax), names))
+                else:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip().split(",")
+                    self.rows.append((float(out[0]), float(out[1]), []))
             except Exception:
                 pass
-            self.stop.wait(0.1)
+            self.stop.wait(0.002 if nv is not None else 0.1)
 
     def __enter__(self):
         self.t.start()
@@ -112,13 +133,11 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n in r[2]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 # --------------------------------------------------------------- helpers
@@ -341,7 +360,7 @@ def main():
     # e2e through the public API: pinned host inputs -> update (H2D) -> enumerate
     # -> estimate -> round (decisions D2H), same metric
     e2e = None
-    if not a.no_e2e and world == 1:
+    if not a.no_e2e:
         pin = {}
         for k in ("c", "w", "act", "bnd", "tpv", "tpn", "job_id", "submit", "ng", "gb", "kst",
                   "n_layers", "layer_off", "cap", "gpn", "mem", "alpha_in", "beta_in", "alpha_x",
@@ -352,20 +371,33 @@ def main():
             setattr(pr, k, tt.numpy())
         h2d = sum(int(t.numel() * t.element_size()) for t in pin.values())
         d2h = pr.n_jobs * 8 + pr.n_types * 4 + 8 + 3 * 8 + (pr.n_jobs + 1) * 4
-        for _ in range(a.warmup):
+
+        def e2e_step():
+            # the user's call sequence: new profiles from host memory -> decisions on host
             cr.update(pr)
             cr.enumerate()
-            cr.schedule_round(cr.estimate(out=mine))
+            if world > 1:
+                pl = sharded.ShardPlan(cr, world)
+                res = sharded.estimate_all(cr, pl, rank, mine=mine, gathered=gathered, full=full)
+            else:
+                res = cr.estimate(out=mine)
+            return cr.schedule_round(res)
+
+        for _ in range(a.warmup):
+            e2e_step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         es, ee = ev(), ev()
         es.record(stream)
         for _ in range(a.steps):
-            cr.update(pr)
-            cr.enumerate()
-            cr.schedule_round(cr.estimate(out=mine))
+            e2e_step()
         ee.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = es.elapsed_time(ee) / a.steps
+        e2e_t = torch.tensor([es.elapsed_time(ee) / a.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(e2e_t.item())
         e2e = {"value": n_plans / (e2e_ms / 1e3), "unit": "cell-plans/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
 
