@@ -237,8 +237,9 @@ crius_status crius_schedule_round_state(crius_ctx *ctx, const crius_cell_result 
  * [1] victim-sequence recomputations, [2] SM cycles in them, [3] SM cycles of
  * Phase A, [4] SM cycles of Phase B, [5] admitted jobs, [6] admissions through
  * ScaleResource, [7] Phase B batches, [8..13] cycle/size breakdown of the
- * sequence passes (setup, same-type pass, other-type pass, reduce+apply, stale
- * caches refreshed, other-type jobs scanned), [14] per-type sequence
+ * sequence recomputations (setup + stale same-type caches, listing, other-type
+ * caches, the per-type move loops, stale caches refreshed, jobs listed for
+ * other-type moves), [14] per-type sequence
  * invalidations, [15..18] cycles of the Phase A
  * batches (window staging, evaluation, ScaleResource incl. sequences, commit).
  * Synchronises `stream`. */

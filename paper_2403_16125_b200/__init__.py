@@ -317,7 +317,7 @@ class Crius:
         _check(lib().crius_round_stats(self.ctx, _ptr(out), _stream_handle(stream)))
         keys = ("phaseA_batches", "seq_recomputes", "seq_cycles", "phaseA_cycles", "phaseB_cycles",
                 "admitted", "scale_admits", "phaseB_batches", "seq_setup_cycles",
-                "seq_same_type_cycles", "seq_other_type_cycles", "seq_reduce_cycles",
+                "seq_listing_cycles", "seq_other_type_cycles", "seq_sequence_cycles",
                 "stale_caches", "other_type_scans", "seq_invalidations", "batch_window_cycles",
                 "batch_eval_cycles", "batch_scale_cycles", "batch_commit_cycles")
         return dict(zip(keys, (int(x) for x in out)))

@@ -36,6 +36,16 @@ def build_debug(out=None):
     return out
 
 
+def build_variant(name, defines):
+    """libcrius compiled with extra -D flags into variants/<name> (experiments only)."""
+    out = os.path.join(ROOT, "variants", name)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [os.environ.get("NVCC", "nvcc")] + NVCC_FLAGS + ["-D" + d for d in defines] + [
+        "-o", out, os.path.join(CSRC, "crius_lib.cu")]
+    subprocess.check_call(cmd)
+    return out
+
+
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB

@@ -95,6 +95,7 @@ struct crius_ctx {
   int64_t *d_round_stats = nullptr;
   int32_t *d_list = nullptr;
   AdmView adm_glob{};  // admitted-job records in global memory (only when they exceed shared)
+  EView eg{};          // (ii) move caches in global memory (rounds listing > kECap jobs)
 };
 
 namespace {
@@ -106,8 +107,8 @@ void free_all(crius_ctx *c) {
                   c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight,
                   c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
-                  c->d_rng, c->d_cur, c->d_free, c->d_total, c->adm_glob.pos,
-                  c->d_round_stats, c->d_score, c->adm_glob.T, c->adm_glob.bi_T,
+                  c->d_rng, c->d_cur, c->d_free, c->d_total, c->eg.loss, c->eg.s2, c->eg.T2,
+                  c->eg.i, c->eg.G2, c->eg.t2, c->d_round_stats, c->d_score, c->adm_glob.T, c->adm_glob.bi_T,
                   c->adm_glob.sc, c->adm_glob.bi_key, c->adm_glob.bi_s, c->adm_glob.pos,
                   c->adm_glob.cur, c->adm_glob.G, c->adm_glob.t, c->adm_glob.nopt,
                   c->adm_glob.bi_opt, c->adm_glob.bi_G2, c->adm_glob.gmin, c->d_list,
@@ -836,6 +837,15 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
     CK(dalloc(&c->adm_glob.gmin, J));
     CK(dalloc(&c->d_list, J));
   }
+  if (!c->eg.i) {
+    CK(dalloc(&c->eg.loss, J));
+    CK(dalloc(&c->eg.s2, J));
+    CK(dalloc(&c->eg.T2, J));
+    CK(dalloc(&c->eg.i, J));
+    CK(dalloc(&c->eg.G2, J));
+    CK(dalloc(&c->eg.t2, J));
+  }
+  R.eg = c->eg;
   CK(cudaFuncSetAttribute(k_round_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   k_round_greedy<<<1, kRoundThreads, dsm, st>>>(R, adm_in_smem, c->adm_glob, win_cap);
   CKL();

@@ -20,8 +20,10 @@
 //    lanes test all options at once and take the kappa-argmin of the successes;
 //  * the victim-move sequence of a trial depends only on the state and on the
 //    option's GPU type t_o (G_o only decides where it is cut), so the greedy
-//    sequence of every type is computed once per state, in parallel over all
-//    admitted jobs, and reused until an admission changes the state.
+//    sequence of every type is computed once per state and reused until an
+//    admission changes it: per-job caches of the best same-type move and of
+//    the best other-type move (staged options in shared memory), then one
+//    group of warps per type runs the d moves with one named barrier per move.
 #pragma once
 #include "common.cuh"
 
@@ -31,6 +33,19 @@ struct OptRec {  // 16 B
   int64_t T;
   int32_t G;
   int32_t t;
+};
+
+// Cached best other-type move (case (ii)) of the listed jobs, entry k of the
+// list: the option with t2 != t and G2 <= free'[t2] of minimum loss = sc - s2
+// (ties -> lowest index); i = -1 if none.  Shared memory up to kECap entries.
+#ifndef CRIUS_ECAP
+#define CRIUS_ECAP 256
+#endif
+constexpr int kECap = CRIUS_ECAP;
+struct EView {
+  double *loss, *s2;
+  int64_t *T2;
+  int32_t *i, *G2, *t2;
 };
 
 struct RoundBuf {
@@ -54,6 +69,7 @@ struct RoundBuf {
   const uint8_t *active;    // [J] by job: the job takes part in this round
   int32_t *run_opt;         // [J] by position: option index of the running Cell, or -1
   int8_t *cand;             // [J] by position: 1 = Phase A candidate (active, not running)
+  EView eg;                 // [J] (ii) caches when more than kECap jobs are listed
 };
 
 __device__ __forceinline__ double score_of(int64_t ref, int64_t T) {
@@ -139,6 +155,21 @@ constexpr int kRoundWarps = kRoundThreads / 32;
 constexpr int kAdmSmem = 2048;  // admitted-job records kept in shared memory up to this many
 constexpr int kAdmBytes = 76;   // bytes per admitted-job record (incl. scratch list)
 
+// Other-type options of the listed jobs, staged in shared memory by the warp
+// that fills their entry (po[k] = offset, pn[k] = count, -1 = not staged:
+// refills then re-read the options from global memory).
+#ifndef CRIUS_POOL
+#define CRIUS_POOL 512
+#endif
+constexpr int kPool = CRIUS_POOL;
+struct OptPool {
+  int64_t *T2;
+  double *s2;
+  int32_t *G2, *ti;  // ti = t2 << 8 | option index
+  int32_t *po, *pn;
+  int32_t *used;
+};
+
 // Admitted jobs, in priority order (SoA; shared memory when they fit, else global).
 // bi_* caches the job's best same-type victim move (case (i) of ScaleResource),
 // which depends only on its current option: bi_opt = -2 marks a stale cache
@@ -170,9 +201,9 @@ struct RoundShared {
   int32_t fr_base[kRT][kRT];  // free counts the sequence was computed from
   int32_t old_fr[kRT];        // free counts before the current commit (thread 0)
   uint32_t changed;           // types changed by the current commit; 0 = no commit
-  long long prof[12];  // cycles: [0] setup+dirty, [1] (i) pass, [2] (ii) pass, [3] reduce+apply; [4] dirty jobs, [5] listed jobs
+  long long prof[12];  // cycles: [0] setup+dirty, [1] listing, [2] (ii) caches, [3] sequences; [4] dirty jobs, [5] listed jobs
   // victim-move sequences, one per GPU type, cut at <= d moves
-  int32_t len[kRT], active[kRT];
+  int32_t len[kRT];
   int32_t mv_a[kRT][kMaxDepth], mv_opt[kRT][kMaxDepth];
   int32_t mv_G[kRT][kMaxDepth], mv_t[kRT][kMaxDepth];  // the victim's new option
   int64_t mv_T[kRT][kMaxDepth];
@@ -185,12 +216,21 @@ struct RoundShared {
   int32_t res_G[kRoundWarps], res_t[kRoundWarps];
   int64_t res_T[kRoundWarps];
   double res_sc[kRoundWarps];
-  // per-(type, warp) best move of the current step, with the move's option data
-  double r_key[kRT][kRoundWarps], r_s2[kRT][kRoundWarps];
-  int64_t r_T2[kRT][kRoundWarps];
-  int32_t r_a[kRT][kRoundWarps], r_i[kRT][kRoundWarps], r_p[kRT][kRoundWarps];
-  int32_t r_freed[kRT][kRoundWarps], r_other[kRT][kRoundWarps];
-  int32_t r_G2[kRT][kRoundWarps], r_t2[kRT][kRoundWarps];
+  // per-warp best move of the current sequence step (type groups of warps,
+  // double-buffered by move parity), each warp's free' and moved jobs
+  double g_key[2][kRoundWarps];
+  uint32_t g_tie[2][kRoundWarps];
+  int32_t g_a[2][kRoundWarps], g_idx[2][kRoundWarps], g_G2[2][kRoundWarps];
+  int32_t g_t2o[2][kRoundWarps], g_freed[2][kRoundWarps];
+  int32_t wf2[kRoundWarps][kRT], wmv[kRoundWarps][kMaxDepth];
+  // cached best other-type moves of the listed jobs (EView, up to kECap)
+  double e_loss[kECap], e_s2[kECap];
+  int64_t e_T2[kECap];
+  int32_t e_i[kECap], e_G2[kECap], e_t2[kECap], e_po[kECap], e_pn[kECap];
+  // their other-type options (OptPool)
+  int64_t p_T2[kPool];
+  double p_s2[kPool];
+  int32_t p_G2[kPool], p_ti[kPool], p_used;
 };
 
 // ---- warp argmin by lexicographic 3-word keys, one redux.sync per word ------
@@ -222,120 +262,309 @@ __device__ __forceinline__ uint32_t kappa_tie(const OptRec &x) {
   return ((uint32_t)ilog2_pow2((uint32_t)x.G) << 8) | (uint32_t)x.t;
 }
 
-// A victim move: key = loss / freed, ordered by (key, admitted index a, option i).
-struct Cand {
-  int have;
-  double key;
-  int a, i, freed, other, G2, t2;
-  int64_t T2;
-  double s2;
-  int p;  // the victim's priority position: ties go to the earlier job (§N6)
-};
-
-__device__ __forceinline__ bool cand_less(const Cand &x, const Cand &y) {
-  if (!x.have) return false;
-  if (!y.have) return true;
-  if (x.key != y.key) return x.key < y.key;
-  if (x.p != y.p) return x.p < y.p;
-  return x.i < y.i;
-}
-
-// Warp-wide argmin of Cands (one per lane) -> winning lane or -1.
-__device__ __forceinline__ int warp_cand_argmin(const Cand &c) {
-  return warp_lex_argmin(c.have, ord_double(c.key), ((uint32_t)c.p << 8) | (uint32_t)c.i);
-}
-
-// Per-(type, warp) best-move slot: written only by the winning lane of its warp.
-__device__ __forceinline__ bool slot_take(RoundShared &sh, int t, int w, const Cand &c) {
-  const int sa = sh.r_a[t][w], sp = sh.r_p[t][w];
-  if (!c.have) return false;
-  if (sa >= 0) {
-    const double sk = sh.r_key[t][w];
-    if (!(c.key < sk || (c.key == sk && (c.p < sp || (c.p == sp && c.i < sh.r_i[t][w])))))
-      return false;
-  }
-  sh.r_key[t][w] = c.key;
-  sh.r_a[t][w] = c.a;
-  sh.r_p[t][w] = c.p;
-  sh.r_i[t][w] = c.i;
-  sh.r_freed[t][w] = c.freed;
-  sh.r_other[t][w] = c.other;
-  sh.r_G2[t][w] = c.G2;
-  sh.r_t2[t][w] = c.t2;
-  sh.r_T2[t][w] = c.T2;
-  sh.r_s2[t][w] = c.s2;
-  return true;
-}
-
 // Warp: refresh the same-type move cache (case (i)) and gmin of admitted job a.
-// Lanes cover the job's options (coalesced 16-byte records, one round trip).
+// The cached move is the job's argmin of key = loss / freed over its same-type
+// options with smaller G, ties -> lowest option index.  Lanes cover the job's
+// options (coalesced 16-byte records and their scores, one round trip).
 __device__ __forceinline__ void refresh_victim_cache(const RoundBuf &R, const AdmView &A, int a) {
   const int lane = threadIdx.x & 31;
   const int v = A.pos[a], cv = A.cur[a], Gc = A.G[a], t = A.t[a], nv = A.nopt[a];
   const double sc = A.sc[a];
-  Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0, v};
+  bool have = false;
+  double bk = 0.0, bs = 0.0;
+  int bi = 0, bG = 0;
+  int64_t bT = 0;
   int gmin = INT32_MAX;
   for (int i2 = lane; i2 < nv; i2 += 32) {
     const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
+    const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
     gmin = min(gmin, o2.G);
     if (i2 == cv || o2.t != t || o2.G >= Gc) continue;
-    const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
-    Cand c{1, __ddiv_rn(sc - s2, (double)(Gc - o2.G)), a, i2, Gc - o2.G, 0, o2.G, o2.t, o2.T, s2, v};
-    if (cand_less(c, best)) best = c;
+    const double k = __ddiv_rn(sc - s2, (double)(Gc - o2.G));
+    if (!have || k < bk) {  // i2 ascending per lane: ties keep the lower index
+      have = true;
+      bk = k;
+      bs = s2;
+      bi = i2;
+      bG = o2.G;
+      bT = o2.T;
+    }
   }
   gmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)gmin);
-  const int src = warp_cand_argmin(best);
+  const int src = warp_lex_argmin(have, ord_double(bk), (uint32_t)bi);
   if (src < 0) {
     if (lane == 0) A.bi_opt[a] = -1;
   } else if (lane == src) {
-    A.bi_opt[a] = best.i;
-    A.bi_key[a] = best.key;
-    A.bi_G2[a] = best.G2;
-    A.bi_T[a] = best.T2;
-    A.bi_s[a] = best.s2;
+    A.bi_opt[a] = bi;
+    A.bi_key[a] = bk;
+    A.bi_G2[a] = bG;
+    A.bi_T[a] = bT;
+    A.bi_s[a] = bs;
   }
   if (lane == 0) A.gmin[a] = gmin;
 }
 
-// Warp: best other-type move (case (ii)) of admitted job a under free' = f2;
-// the winning lane offers it to the (type, warp) slot.  freed = G_cur is a
-// power of two, so key = loss * 2^-log2(G_cur) exactly: the minimum key is the
-// minimum rounded loss (ties -> lowest option index), one division.
-__device__ __forceinline__ void other_type_move(RoundShared &sh, const RoundBuf &R,
-                                                const AdmView &A, int a, const int32_t *f2) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int v = A.pos[a], Gc = A.G[a], t = A.t[a], nv = A.nopt[a];
+// Warp: fill entry k for admitted job a under free' = f2 (lanes over options)
+// and stage the job's other-type options in the pool when it has room.
+__device__ __forceinline__ void other_type_best_warp(const RoundBuf &R, const AdmView &A, int a,
+                                                     const int32_t *f2, const EView &E, int k,
+                                                     const OptPool *pool) {
+  const int lane = threadIdx.x & 31;
+  const int v = A.pos[a], t = A.t[a], nv = A.nopt[a];
   const double sc = A.sc[a];
-  Cand best{0, 0.0, a, 0, 0, 0, 0, 0, 0, 0.0, v};
-  for (int i2 = lane; i2 < nv; i2 += 32) {
-    const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
-    if (o2.t == t || o2.G > f2[o2.t]) continue;
-    const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
-    Cand c{1, sc - s2, a, i2, Gc, 1, o2.G, o2.t, o2.T, s2, v};  // key holds the loss here
-    if (cand_less(c, best)) best = c;
+  int off = -1;
+  if (pool) {
+    if (lane == 0) {
+      off = atomicAdd(pool->used, nv);
+      if (off + nv > kPool) off = -1;
+    }
+    off = __shfl_sync(0xffffffffu, off, 0);
   }
-  const int src = warp_cand_argmin(best);
-  if (lane == src) {
-    best.key = __ddiv_rn(best.key, (double)Gc);
-    slot_take(sh, t, wid, best);
+  int cnt = 0;
+  bool have = false;
+  double bl = 0.0, bs = 0.0;
+  int bi = 0, bG = 0, bt = 0;
+  int64_t bT = 0;
+  for (int i0 = 0; i0 < nv; i0 += 32) {
+    const int i2 = i0 + lane;
+    OptRec o2{0, 0, t};
+    double s2 = 0.0;
+    if (i2 < nv) {
+      o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
+      s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
+    }
+    const bool oth = i2 < nv && o2.t != t;
+    if (off >= 0) {
+      const unsigned bm = __ballot_sync(0xffffffffu, oth);
+      if (oth) {
+        const int q = off + cnt + __popc(bm & ((1u << lane) - 1));
+        pool->T2[q] = o2.T;
+        pool->s2[q] = s2;
+        pool->G2[q] = o2.G;
+        pool->ti[q] = (o2.t << 8) | i2;
+      }
+      cnt += __popc(bm);
+    }
+    if (!oth || o2.G > f2[o2.t]) continue;
+    const double l = sc - s2;
+    if (!have || l < bl) {
+      have = true;
+      bl = l;
+      bs = s2;
+      bi = i2;
+      bG = o2.G;
+      bt = o2.t;
+      bT = o2.T;
+    }
   }
-  __syncwarp();
+  if (pool && lane == 0) {
+    pool->po[k] = off;
+    pool->pn[k] = cnt;
+  }
+  const int src = warp_lex_argmin(have, ord_double(bl), (uint32_t)bi);
+  if (src < 0) {
+    if (lane == 0) E.i[k] = -1;
+  } else if (lane == src) {
+    E.i[k] = bi;
+    E.loss[k] = bl;
+    E.s2[k] = bs;
+    E.G2[k] = bG;
+    E.t2[k] = bt;
+    E.T2[k] = bT;
+  }
 }
 
-// All threads: the greedy victim sequence of every GPU type t from the current
-// state (the §N6 ScaleResource move loop run for d moves without the G_o stop;
-// an option on type t uses the shortest prefix that frees G_o).  Each admitted
-// job is a candidate only for the sequence of its own current type.  Per move,
-// in one pass: cached same-type moves of every job (shared memory only), and
-// other-type moves of the few jobs whose smallest option could fit free'[t2].
+// One lane: recompute entry k after a (ii) move took GPUs its option needed
+// (free' only decreases for the other types along a sequence); options from
+// the pool (shared memory) when staged, else from global memory.
+__device__ __forceinline__ int other_type_best_lane(const RoundBuf &R, const AdmView &A, int a,
+                                                    const int32_t *f2, const EView &E, int k,
+                                                    const OptPool *pool) {
+  const double sc = A.sc[a];
+  int bi = -1;
+  double bl = 0.0;
+  const int off = pool ? pool->po[k] : -1;
+  if (off >= 0) {  // other-type options in index order
+    const int n = pool->pn[k];
+    int bq = -1;
+    for (int q = off; q < off + n; ++q) {
+      const int ti = pool->ti[q], G2 = pool->G2[q];
+      if (G2 > f2[ti >> 8]) continue;
+      const double l = sc - pool->s2[q];
+      if (bi < 0 || l < bl) {
+        bi = ti & 0xff;
+        bl = l;
+        bq = q;
+      }
+    }
+    if (bq >= 0) {
+      E.loss[k] = bl;
+      E.s2[k] = pool->s2[bq];
+      E.G2[k] = pool->G2[bq];
+      E.t2[k] = pool->ti[bq] >> 8;
+      E.T2[k] = pool->T2[bq];
+    }
+    E.i[k] = bi;
+    return bi;
+  }
+  const int v = A.pos[a], t = A.t[a], nv = A.nopt[a];
+#pragma unroll 4
+  for (int i2 = 0; i2 < nv; ++i2) {
+    const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
+    const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
+    if (o2.t == t || o2.G > f2[o2.t]) continue;
+    const double l = sc - s2;
+    if (bi < 0 || l < bl) {
+      bi = i2;
+      bl = l;
+      E.loss[k] = l;
+      E.s2[k] = s2;
+      E.G2[k] = o2.G;
+      E.t2[k] = o2.t;
+      E.T2[k] = o2.T;
+    }
+  }
+  E.i[k] = bi;
+  return bi;
+}
+
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Warps [t*gw, (t+1)*gw): the greedy victim sequence of GPU type t (the §N6
+// ScaleResource move loop run for d moves without the G_o stop; an option on
+// type t later uses the shortest prefix that frees G_o).  Per move, the argmin
+// of (key, priority position, option) over the unmoved type-t jobs' cached
+// same-type moves (i) and the listed jobs' cached other-type moves (ii),
+// key = loss / freed.  One named barrier (1 + t) per move: every warp reduces
+// the group's per-warp winners itself (slots double-buffered by move parity)
+// and keeps its own copy of free' and of the moved jobs; the group's first
+// warp records the sequence.
+__device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView &A,
+                              const int32_t *list, int nE, const EView &E, const OptPool *pool,
+                              int t, int gw) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gwid = wid - t * gw, gt = gwid * 32 + lane, gn = gw * 32, w0 = t * gw;
+  const int n_adm = sh.n_adm, TT = R.T;
+  int32_t *f2 = sh.wf2[wid];
+  int32_t *mv = sh.wmv[wid];
+  if (lane < TT) f2[lane] = sh.frs[t][0][lane];
+  __syncwarp();
+  for (int m = 0; m < R.depth; ++m) {
+    bool have = false;
+    double bk = 0.0;
+    int bp = 0, bi = 0, ba = -1, bidx = -1;
+    for (int a = gt; a < n_adm; a += gn) {  // (i)
+      if (A.t[a] != t) continue;
+      const int bo = A.bi_opt[a];
+      if (bo < 0) continue;
+      bool moved = false;
+      for (int q = 0; q < m; ++q) moved |= mv[q] == a;
+      if (moved) continue;
+      const double k = A.bi_key[a];
+      const int p = A.pos[a];
+      if (!have || k < bk || (k == bk && (p < bp || (p == bp && bo < bi)))) {
+        have = true;
+        bk = k;
+        bp = p;
+        bi = bo;
+        ba = a;
+        bidx = -1;
+      }
+    }
+    for (int k = gt; k < nE; k += gn) {  // (ii)
+      const int a = list[k];
+      if (A.t[a] != t) continue;
+      bool moved = false;
+      for (int q = 0; q < m; ++q) moved |= mv[q] == a;
+      if (moved) continue;
+      int ei = E.i[k];
+      if (ei >= 0 && E.G2[k] > f2[E.t2[k]]) ei = other_type_best_lane(R, A, a, f2, E, k, pool);
+      if (ei < 0) continue;
+      const double key = __ddiv_rn(E.loss[k], (double)A.G[a]);
+      const int p = A.pos[a];
+      if (!have || key < bk || (key == bk && (p < bp || (p == bp && ei < bi)))) {
+        have = true;
+        bk = key;
+        bp = p;
+        bi = ei;
+        ba = a;
+        bidx = k;
+      }
+    }
+    const uint32_t tie = ((uint32_t)bp << 8) | (uint32_t)bi;
+    const int src = warp_lex_argmin(have, ord_double(bk), tie);
+    const int par = m & 1;
+    if (lane == 0) sh.g_a[par][wid] = -1;
+    __syncwarp();
+    if (lane == src) {
+      int G2, t2o, freed;
+      if (bidx < 0) {
+        G2 = A.bi_G2[ba];
+        t2o = t;
+        freed = A.G[ba] - G2;
+      } else {
+        G2 = E.G2[bidx];
+        t2o = E.t2[bidx] | 0x100;
+        freed = A.G[ba];
+      }
+      sh.g_key[par][wid] = bk;
+      sh.g_tie[par][wid] = tie;
+      sh.g_a[par][wid] = ba;
+      sh.g_idx[par][wid] = bidx;
+      sh.g_G2[par][wid] = G2;
+      sh.g_t2o[par][wid] = t2o;
+      sh.g_freed[par][wid] = freed;
+    }
+    group_bar(1 + t, gn);
+    // every warp: the group's winner (lanes < gw hold the per-warp winners)
+    const int w = w0 + lane;
+    const bool in = lane < gw && sh.g_a[par][w] >= 0;
+    const int wl = warp_lex_argmin(in, ord_double(in ? sh.g_key[par][w] : 0.0),
+                                   in ? sh.g_tie[par][w] : 0u);
+    if (wl < 0) break;
+    const int ws = w0 + wl;
+    const int ca = sh.g_a[par][ws], t2o = sh.g_t2o[par][ws], G2 = sh.g_G2[par][ws];
+    const int t2 = t2o & 0xff, other = t2o >> 8;
+    if (lane < TT) {
+      int f = f2[lane];
+      if (lane == t) f += sh.g_freed[par][ws];
+      if (lane == t2 && other) f -= G2;
+      f2[lane] = f;
+      if (gwid == 0) sh.frs[t][m + 1][lane] = f;
+    }
+    if (lane == 0) mv[m] = ca;
+    if (gwid == 0 && lane == 0) {  // record move m
+      const int idx = sh.g_idx[par][ws];
+      const double s2 = idx < 0 ? A.bi_s[ca] : E.s2[idx];
+      sh.mv_a[t][m] = ca;
+      sh.mv_opt[t][m] = (int)(sh.g_tie[par][ws] & 0xff);
+      sh.mv_G[t][m] = G2;
+      sh.mv_t[t][m] = t2;
+      sh.mv_T[t][m] = idx < 0 ? A.bi_T[ca] : E.T2[idx];
+      sh.mv_sc[t][m] = s2;
+      sh.cum[t][m + 1] = __dadd_rn(sh.cum[t][m], A.sc[ca] - s2);
+      sh.len[t] = m + 1;
+    }
+    __syncwarp();
+  }
+}
+
+// All threads: the victim sequences of every stale GPU type from the current
+// state.  (1) refresh the stale same-type caches (one warp per job); (2) list
+// the jobs that may have an other-type move (smallest option G <= the largest
+// free count of another type -- free' of the other types only decreases along
+// a sequence, so this superset holds for every move); (3) their best
+// other-type move under the current free counts (one warp per job); (4) one
+// warp per stale type runs its d moves from shared-memory caches only.
 __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmView &A,
-                                 int32_t *list) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+                                 int32_t *list, const EView &Es) {
+  const int tid = threadIdx.x, wid = tid >> 5;
   const int TT = R.T, n_adm = sh.n_adm;
   if (tid < TT) {
     const int c = !sh.seq_ok[tid];
     sh.comp[tid] = c;
-    sh.active[tid] = c;
     if (c) {
       sh.len[tid] = 0;
       sh.cum[tid][0] = 0.0;
@@ -350,16 +579,19 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
     sh.frs[tid / TT][0][tid % TT] = sh.fr[tid % TT];
     sh.fr_base[tid / TT][tid % TT] = sh.fr[tid % TT];
   }
-  if (lane < TT) sh.r_a[lane][wid] = -1;
-  if (tid == 0) sh.n_dirty = 0;
+  if (tid == 0) {
+    sh.n_dirty = 0;
+    sh.p_used = 0;
+  }
   long long t0 = clock64();
   __syncthreads();
-  // stale same-type caches -> list -> one warp per job
+  // (1) stale same-type caches -> list -> one warp per job
   for (int a = tid; a < n_adm; a += kRoundThreads)
     if (A.bi_opt[a] == -2) list[atomicAdd(&sh.n_dirty, 1)] = a;
   CRIUS_CHECK(n_adm <= R.J);
   __syncthreads();
   for (int k = wid; k < sh.n_dirty; k += kRoundWarps) refresh_victim_cache(R, A, list[k]);
+  if (tid == 0) sh.n_list = 0;
   __syncthreads();
   if (tid == 0) {
     const long long t1 = clock64();
@@ -367,89 +599,45 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
     sh.prof[4] += sh.n_dirty;
     t0 = t1;
   }
-
-  for (int m = 0; m < R.depth; ++m) {
-    if (tid == 0) sh.n_list = 0;
-    __syncthreads();
-    for (int a0 = 0; a0 < n_adm; a0 += kRoundThreads) {
-      const int a = a0 + tid;
-      Cand mine{0, 0.0, 0, 0, 0, 0, 0, 0, 0, 0.0, 0};
-      int myt = -1;
-      if (a < n_adm) {
-        myt = A.t[a];
-        if (m == 0 && sh.comp[myt]) atomicMin(&sh.gmin_type[myt], A.gmin[a]);
-        bool moved = !sh.active[myt];
-        for (int q = 0; q < m; ++q) moved |= sh.mv_a[myt][q] == a;
-        if (!moved) {
-          const int bo = A.bi_opt[a];
-          if (bo >= 0)
-            mine = Cand{1, A.bi_key[a], a, bo, A.G[a] - A.bi_G2[a], 0, A.bi_G2[a], myt, A.bi_T[a],
-                        A.bi_s[a], A.pos[a]};
-          if (A.gmin[a] <= sh.fmax_other[myt]) list[atomicAdd(&sh.n_list, 1)] = a;
-        }
-      }
-      // (i) cached same-type moves: per type, the warp's winner offers itself
-      for (int t = 0; t < TT; ++t) {
-        const bool v = myt == t && mine.have;
-        const int src = warp_lex_argmin(v, ord_double(mine.key), ((uint32_t)mine.p << 8) | (uint32_t)mine.i);
-        if (lane == src) slot_take(sh, t, wid, mine);
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    // (ii) other-type moves of the listed jobs, one warp per job (balanced)
-    for (int k = wid; k < sh.n_list; k += kRoundWarps) {
-      const int aa = list[k];
-      other_type_move(sh, R, A, aa, sh.frs[A.t[aa]][m]);
-    }
-    if (tid == 0) sh.prof[5] += sh.n_list;
-    __syncthreads();
-    if (tid == 0) {
-      const long long t1 = clock64();
-      sh.prof[1] += t1 - t0;
-      t0 = t1;
-    }
-    if (wid < TT && sh.active[wid]) {  // warp t reduces type t, applies its move, preps m+1
-      const int t = wid;
-      const bool in = lane < kRoundWarps;
-      const int ra = in ? sh.r_a[t][lane] : -1;
-      const int rp = in ? sh.r_p[t][lane] : 0;
-      const int src = warp_lex_argmin(ra >= 0, ord_double(in ? sh.r_key[t][lane] : 0.0),
-                                      ((uint32_t)rp << 8) | (uint32_t)(in ? sh.r_i[t][lane] : 0));
-      if (src < 0) {
-        if (lane == 0) sh.active[t] = 0;
-      } else {
-        if (lane == 0) {
-          const int ca = sh.r_a[t][src];
-          sh.mv_a[t][m] = ca;
-          sh.mv_opt[t][m] = sh.r_i[t][src];
-          sh.mv_G[t][m] = sh.r_G2[t][src];
-          sh.mv_t[t][m] = sh.r_t2[t][src];
-          sh.mv_T[t][m] = sh.r_T2[t][src];
-          sh.mv_sc[t][m] = sh.r_s2[t][src];
-          const double loss = A.sc[ca] - sh.r_s2[t][src];
-          sh.cum[t][m + 1] = __dadd_rn(sh.cum[t][m], loss);
-          int fm = -1;
-          for (int q = 0; q < TT; ++q) {
-            int f = sh.frs[t][m][q];
-            if (q == t) f += sh.r_freed[t][src];
-            if (q == sh.r_t2[t][src] && sh.r_other[t][src]) f -= sh.r_G2[t][src];
-            sh.frs[t][m + 1][q] = f;
-            if (q != t) fm = max(fm, f);
-          }
-          sh.fmax_other[t] = fm;
-          sh.len[t] = m + 1;
-        }
-        __syncwarp();
-        if (lane < kRoundWarps) sh.r_a[t][lane] = -1;  // reset this type's slots for move m + 1
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const long long t1 = clock64();
-      sh.prof[3] += t1 - t0;
-      t0 = t1;
-    }
+  // (2) gmin per type; listed jobs
+  for (int a = tid; a < n_adm; a += kRoundThreads) {
+    const int myt = A.t[a];
+    if (!sh.comp[myt]) continue;
+    const int g = A.gmin[a];
+    atomicMin(&sh.gmin_type[myt], g);
+    if (g <= sh.fmax_other[myt]) list[atomicAdd(&sh.n_list, 1)] = a;
+  }
+  __syncthreads();
+  const int nE = sh.n_list;
+  const EView E = nE <= kECap ? Es : R.eg;
+  if (tid == 0) {
+    const long long t1 = clock64();
+    sh.prof[1] += t1 - t0;
+    sh.prof[5] += nE;
+    t0 = t1;
+  }
+  // (3) best other-type move of each listed job under the current free counts
+  OptPool pl{sh.p_T2, sh.p_s2, sh.p_G2, sh.p_ti, sh.e_po, sh.e_pn, &sh.p_used};
+  const OptPool *pool = nE <= kECap ? &pl : nullptr;
+  for (int k = wid; k < nE; k += kRoundWarps) other_type_best_warp(R, A, list[k], sh.fr, E, k, pool);
+  __syncthreads();
+  if (tid == 0) {
+    const long long t1 = clock64();
+    sh.prof[2] += t1 - t0;
+    t0 = t1;
+  }
+  // (4) one warp per stale type
+  {
+#ifndef CRIUS_SEQ_WARPS
+#define CRIUS_SEQ_WARPS 32
+#endif
+    const int gw = min(CRIUS_SEQ_WARPS, kRoundWarps / TT), t = wid / gw;  // warps per type
+    if (t < TT && sh.comp[t]) type_sequence(sh, R, A, list, nE, E, pool, t, gw);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const long long t1 = clock64();
+    sh.prof[3] += t1 - t0;
   }
   if (tid < TT && sh.comp[tid]) sh.seq_ok[tid] = 1;
   __syncthreads();
@@ -647,7 +835,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       for (int q = 0; q < TT; ++q) stale |= !sh.seq_ok[q];
       if (stale) {
         const long long c0 = clock64();
-        compute_all_seqs(sh, R, A, list);
+        compute_all_seqs(sh, R, A, list,
+                         EView{sh.e_loss, sh.e_s2, sh.e_T2, sh.e_i, sh.e_G2, sh.e_t2});
         c_seq += clock64() - c0;
         ++n_seq;
       }
