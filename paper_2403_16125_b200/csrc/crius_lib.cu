@@ -107,7 +107,7 @@ void free_all(crius_ctx *c) {
                   c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight,
                   c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
-                  c->d_rng, c->d_cur, c->d_free, c->d_total, c->eg.loss, c->eg.s2, c->eg.T2,
+                  c->d_rng, c->d_cur, c->d_free, c->d_total, c->eg.loss, c->eg.s2, c->eg.key, c->eg.T2,
                   c->eg.i, c->eg.G2, c->eg.t2, c->d_round_stats, c->d_score, c->adm_glob.T, c->adm_glob.bi_T,
                   c->adm_glob.sc, c->adm_glob.bi_key, c->adm_glob.bi_s, c->adm_glob.pos,
                   c->adm_glob.cur, c->adm_glob.G, c->adm_glob.t, c->adm_glob.nopt,
@@ -840,6 +840,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   if (!c->eg.i) {
     CK(dalloc(&c->eg.loss, J));
     CK(dalloc(&c->eg.s2, J));
+    CK(dalloc(&c->eg.key, J));
     CK(dalloc(&c->eg.T2, J));
     CK(dalloc(&c->eg.i, J));
     CK(dalloc(&c->eg.G2, J));

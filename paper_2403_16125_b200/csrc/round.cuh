@@ -43,7 +43,7 @@ struct OptRec {  // 16 B
 #endif
 constexpr int kECap = CRIUS_ECAP;
 struct EView {
-  double *loss, *s2;
+  double *loss, *s2, *key;  // key = loss / G_cur (the move's ScaleResource key)
   int64_t *T2;
   int32_t *i, *G2, *t2;
 };
@@ -224,7 +224,7 @@ struct RoundShared {
   int32_t g_t2o[2][kRoundWarps], g_freed[2][kRoundWarps];
   int32_t wf2[kRoundWarps][kRT], wmv[kRoundWarps][kMaxDepth];
   // cached best other-type moves of the listed jobs (EView, up to kECap)
-  double e_loss[kECap], e_s2[kECap];
+  double e_loss[kECap], e_s2[kECap], e_key[kECap];
   int64_t e_T2[kECap];
   int32_t e_i[kECap], e_G2[kECap], e_t2[kECap], e_po[kECap], e_pn[kECap];
   // their other-type options (OptPool)
@@ -367,6 +367,7 @@ __device__ __forceinline__ void other_type_best_warp(const RoundBuf &R, const Ad
   } else if (lane == src) {
     E.i[k] = bi;
     E.loss[k] = bl;
+    E.key[k] = __ddiv_rn(bl, (double)A.G[a]);
     E.s2[k] = bs;
     E.G2[k] = bG;
     E.t2[k] = bt;
@@ -399,6 +400,7 @@ __device__ __forceinline__ int other_type_best_lane(const RoundBuf &R, const Adm
     }
     if (bq >= 0) {
       E.loss[k] = bl;
+      E.key[k] = __ddiv_rn(bl, (double)A.G[a]);
       E.s2[k] = pool->s2[bq];
       E.G2[k] = pool->G2[bq];
       E.t2[k] = pool->ti[bq] >> 8;
@@ -424,6 +426,7 @@ __device__ __forceinline__ int other_type_best_lane(const RoundBuf &R, const Adm
       E.T2[k] = o2.T;
     }
   }
+  if (bi >= 0) E.key[k] = __ddiv_rn(bl, (double)A.G[a]);
   E.i[k] = bi;
   return bi;
 }
@@ -455,15 +458,12 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     bool have = false;
     double bk = 0.0;
     int bp = 0, bi = 0, ba = -1, bidx = -1;
-    for (int a = gt; a < n_adm; a += gn) {  // (i)
-      if (A.t[a] != t) continue;
-      const int bo = A.bi_opt[a];
-      if (bo < 0) continue;
+    for (int a = gt; a < n_adm; a += gn) {  // (i): loads issued together
+      const int ta = A.t[a], bo = A.bi_opt[a], p = A.pos[a];
+      const double k = A.bi_key[a];
       bool moved = false;
       for (int q = 0; q < m; ++q) moved |= mv[q] == a;
-      if (moved) continue;
-      const double k = A.bi_key[a];
-      const int p = A.pos[a];
+      if (ta != t || bo < 0 || moved) continue;
       if (!have || k < bk || (k == bk && (p < bp || (p == bp && bo < bi)))) {
         have = true;
         bk = k;
@@ -475,15 +475,17 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     }
     for (int k = gt; k < nE; k += gn) {  // (ii)
       const int a = list[k];
-      if (A.t[a] != t) continue;
+      const int ta = A.t[a], p = A.pos[a], G2 = E.G2[k], t2 = E.t2[k];
+      int ei = E.i[k];
+      double key = E.key[k];
       bool moved = false;
       for (int q = 0; q < m; ++q) moved |= mv[q] == a;
-      if (moved) continue;
-      int ei = E.i[k];
-      if (ei >= 0 && E.G2[k] > f2[E.t2[k]]) ei = other_type_best_lane(R, A, a, f2, E, k, pool);
+      if (ta != t || moved) continue;
+      if (ei >= 0 && G2 > f2[t2]) {
+        ei = other_type_best_lane(R, A, a, f2, E, k, pool);
+        key = E.key[k];
+      }
       if (ei < 0) continue;
-      const double key = __ddiv_rn(E.loss[k], (double)A.G[a]);
-      const int p = A.pos[a];
       if (!have || key < bk || (key == bk && (p < bp || (p == bp && ei < bi)))) {
         have = true;
         bk = key;
@@ -836,7 +838,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       if (stale) {
         const long long c0 = clock64();
         compute_all_seqs(sh, R, A, list,
-                         EView{sh.e_loss, sh.e_s2, sh.e_T2, sh.e_i, sh.e_G2, sh.e_t2});
+                         EView{sh.e_loss, sh.e_s2, sh.e_key, sh.e_T2, sh.e_i, sh.e_G2, sh.e_t2});
         c_seq += clock64() - c0;
         ++n_seq;
       }
