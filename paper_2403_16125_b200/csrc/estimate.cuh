@@ -442,17 +442,25 @@ __device__ __forceinline__ void warp_prefix32(int64_t *dst, const int32_t *src, 
 
 // K2 rows f[2..smax] (lowest-argmin binary search, §N3), in the narrowest
 // integer type that holds P[L] (every f value is <= P[L]): exact either way.
+// The searched crossing lo(s, i) = first k with f[s-1][k] + P[k] >= P[i] can
+// only move right with s (f[s-1][k] <= f[s-2][k]: one more stage never raises
+// the min-max), so row s searches [max(s-1, lo(s-1, i)), i] -- the bounds are
+// kept in ARG row 0, which the backtrack never reads.
 template <typename V>
 __device__ __forceinline__ void stage_dp(const V *P0, V *F0, V *F1, uint8_t *ARG, int Lp, int L,
                                          int smax, int lane) {
-  for (int i = lane; i <= L; i += 32) F0[i] = P0[i];
+  uint8_t *LOB = ARG;  // row 0: lo(s-1, i)
+  for (int i = lane; i <= L; i += 32) {
+    F0[i] = P0[i];
+    LOB[i] = 0;
+  }
   __syncwarp();
   V *fp = F0, *fc = F1;
   for (int s = 2; s <= smax; ++s) {
     uint8_t *arow = ARG + s * Lp;
     for (int i = s + lane; i <= L; i += 32) {
       const V Pi = P0[i];
-      int lo = s - 1, hi = i;  // first k in [s-1, i-1] with f[s-1][k] >= P[i]-P[k], else i
+      int lo = max(s - 1, (int)LOB[i]), hi = i;  // first k in [lo, i-1] with f[s-1][k] >= P[i]-P[k], else i
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (fp[mid] >= Pi - P0[mid])
@@ -483,6 +491,7 @@ __device__ __forceinline__ void stage_dp(const V *P0, V *F0, V *F1, uint8_t *ARG
       }
       fc[i] = val;
       arow[i] = (uint8_t)a;
+      LOB[i] = (uint8_t)lo;
     }
     __syncwarp();
     V *tmp = fp;
