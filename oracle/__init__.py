@@ -166,6 +166,44 @@ class Oracle:
             "tune_assembled")
         return t_ns, bidx, sk.reshape(c1 - c0, kstride)
 
+    def paper_stages(self, j, t, G, S):
+        """NEXT-2: (cuts bounds[S+1], GPUs per stage g[S]) of Cell (j, t, G, S)."""
+        b = np.zeros(S + 1, np.int32)
+        g = np.zeros(S, np.int32)
+        self._check(self.L.oracle_paper_stages(C.byref(self.s), j, t, G, S, _ptr(b), _ptr(g)),
+                    "paper_stages")
+        return b, g
+
+    def paper_fractional(self, j, t, G, S, bounds):
+        """NEXT-2: fractional GPUs G F_s / F of the stages of `bounds` as (num[S], den)."""
+        b = np.ascontiguousarray(bounds, np.int32)
+        num = np.zeros(S, np.int64)
+        den = C.c_int64()
+        self._check(self.L.oracle_paper_fractional(C.byref(self.s), j, t, G, S, _ptr(b), _ptr(num),
+                                                   C.byref(den)), "paper_fractional")
+        return num, den.value
+
+    def paper_plan_cost(self, j, t, S, bounds, g, p):
+        b = np.ascontiguousarray(bounds, np.int32)
+        gg = np.ascontiguousarray(g, np.int32)
+        ti, fe = C.c_int64(), C.c_int32()
+        self._check(self.L.oracle_paper_plan_cost(C.byref(self.s), j, t, S, _ptr(b), _ptr(gg), p,
+                                                  C.byref(ti), C.byref(fe)), "paper_plan_cost")
+        return ti.value, bool(fe.value)
+
+    def estimate_paper(self, cells, c0=0, c1=None, kstride=None):
+        n = len(cells["job"])
+        c1 = n if c1 is None else c1
+        kstride = int(cells["S"].max()) if kstride is None else kstride
+        t_ns = np.zeros(c1 - c0, np.int64)
+        plan = np.zeros(c1 - c0, np.int32)
+        lg = np.zeros((c1 - c0) * kstride, np.int8)
+        self._check(self.L.oracle_estimate_paper(
+            C.byref(self.s), *[_ptr(cells[k]) for k in ("job", "type", "G", "S")],
+            C.c_int64(c0), C.c_int64(c1), _ptr(t_ns), _ptr(plan), _ptr(lg), kstride),
+            "estimate_paper")
+        return t_ns, plan, lg.reshape(c1 - c0, kstride)
+
     def round_state(self, cells, t_ns, free_in, run_cell=None, active=None):
         J, T = self.pr.n_jobs, self.pr.n_types
         dec = np.zeros(J, np.int64)
@@ -205,6 +243,14 @@ def tune_choices(g, tp_favour):
     ks = np.zeros(16, np.int32)
     n = lib().oracle_tune_choices(g, int(tp_favour), _ptr(ks))
     return [int(k) for k in ks[:n]]
+
+
+def paper_round_pow2(num, den):
+    """NEXT-2: num/den rounded to the nearest power of two (ties up, >= 1)."""
+    f = lib().oracle_paper_round_pow2
+    f.restype = C.c_int32
+    f.argtypes = [C.c_int64, C.c_int64]
+    return int(f(num, den))
 
 
 def comm(kind, p, alpha, beta, V, n=1):

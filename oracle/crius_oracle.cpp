@@ -273,6 +273,172 @@ i128 assembled_latency(const std::vector<StageCost> &st, int32_t B, int32_t form
   return sum + (i128)(B - 1) * (mx - (form == 1 ? tc : 0)) + sy;
 }
 
+// ---- NEXT-2: the paper's stage determination (Fig. stage_partition)
+// Reading R-8 (cuts): the model is cut at the S-1 inter-layer gaps with the
+// smallest boundary bytes ("selects the smallest 3 inter-operator
+// communication as the clustering boundaries").  With beta = the
+// (S-1)-th smallest gap byte count, every gap below beta is a cut and the rest
+// are chosen among the gaps equal to beta; among those cut sets, the one that
+// keeps the stages' computation most similar: min-max of the tp=1
+// per-sample compute, lowest argmin at every step (the R0 rule of §N3).
+// Gap q (1 <= q <= L-1) lies between layers q-1 and q and carries bnd[q-1].
+std::vector<int32_t> paper_cuts(const oracle_problem *pr, int32_t j, int32_t t, int32_t S) {
+  const int32_t L = pr->n_layers[j];
+  const int64_t off = pr->layer_off[j];
+  const int64_t TL = pr->layer_off[pr->n_jobs];
+  const int32_t *c0 = pr->c + ((int64_t)t * (pr->k_max + 1) + 0) * TL + off;
+  std::vector<int32_t> b(S + 1);
+  b[0] = 0;
+  b[S] = L;
+  if (S == 1) return b;
+  std::vector<int64_t> bytes;
+  for (int32_t q = 1; q < L; ++q) bytes.push_back(pr->bnd[off + q - 1]);
+  std::vector<int64_t> sorted = bytes;
+  std::sort(sorted.begin(), sorted.end());
+  const int64_t beta = sorted[S - 2];
+  auto forced = [&](int32_t q) { return q >= 1 && q < L && bytes[q - 1] < beta; };
+  auto allowed = [&](int32_t q) { return q >= 1 && q < L && bytes[q - 1] <= beta; };
+  // no forced gap strictly inside (k, i)
+  auto clear = [&](int32_t k, int32_t i) {
+    for (int32_t q = k + 1; q < i; ++q)
+      if (forced(q)) return false;
+    return true;
+  };
+  auto stage = [&](int32_t k, int32_t i) {  // tp=1 compute of layers [k, i), summed directly
+    int64_t v = 0;
+    for (int32_t l = k; l < i; ++l) v += c0[l];
+    return v;
+  };
+  std::vector<std::vector<int64_t>> f(S + 1, std::vector<int64_t>(L + 1, INF));
+  std::vector<std::vector<int32_t>> arg(S + 1, std::vector<int32_t>(L + 1, -1));
+  for (int32_t i = 1; i <= L; ++i)
+    if ((allowed(i) || i == L) && clear(0, i)) f[1][i] = stage(0, i);
+  for (int32_t s = 2; s <= S; ++s)
+    for (int32_t i = s; i <= L; ++i) {
+      if (!(allowed(i) || i == L)) continue;
+      for (int32_t k = s - 1; k <= i - 1; ++k) {
+        if (!allowed(k) || f[s - 1][k] == INF || !clear(k, i)) continue;
+        const int64_t v = std::max(f[s - 1][k], stage(k, i));
+        if (v < f[s][i]) {
+          f[s][i] = v;
+          arg[s][i] = k;
+        }
+      }
+    }
+  for (int32_t s = S; s >= 2; --s) b[s - 1] = arg[s][b[s]];
+  return b;
+}
+
+// Reading R-9 (GPUs per stage): stage s maps G * F_s / F GPUs (F = tp=1
+// compute, the FLOP proxy of A-3; "T_elapsed = FLOPs / Number_GPU"),
+// rounded to the nearest power of two (linear distance, ties up, at least 1;
+// "approximates a power of 2"); conservation repair: while the sum
+// exceeds G halve the stage with the lowest F_s/g_s among g_s >= 2, then while
+// it is below G double the stage with the highest F_s/g_s among those that
+// keep the sum <= G (ties: earliest stage).
+// Nearest power of two to x = num / den (linear distance, ties up), at least 1.
+int32_t round_pow2(i128 num, i128 den) {
+  if (num < den) return 1;
+  int32_t a = 0;
+  while (((i128)2 << a) * den <= num) ++a;  // 2^a <= x < 2^(a+1)
+  return (2 * num >= 3 * ((i128)1 << a) * den) ? (2 << a) : (1 << a);
+}
+
+std::vector<int32_t> paper_gpus(const oracle_problem *pr, int32_t j, int32_t t, int32_t G,
+                                const std::vector<int32_t> &b) {
+  const int32_t S = (int32_t)b.size() - 1;
+  const int64_t off = pr->layer_off[j];
+  const int64_t TL = pr->layer_off[pr->n_jobs];
+  const int32_t *c0 = pr->c + ((int64_t)t * (pr->k_max + 1) + 0) * TL + off;
+  std::vector<i128> F(S, 0);
+  i128 Ftot = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    for (int32_t l = b[s]; l < b[s + 1]; ++l) F[s] += c0[l];
+    Ftot += F[s];
+  }
+  std::vector<int32_t> g(S);
+  for (int32_t s = 0; s < S; ++s) g[s] = round_pow2((i128)G * F[s], Ftot);  // x = G F_s / F
+  auto sum = [&]() {
+    int64_t v = 0;
+    for (int32_t x : g) v += x;
+    return v;
+  };
+  while (sum() > G) {
+    int32_t w = -1;
+    for (int32_t s = 0; s < S; ++s)
+      if (g[s] >= 2 && (w < 0 || F[s] * g[w] < F[w] * g[s])) w = s;
+    g[w] /= 2;
+  }
+  while (sum() < G) {
+    int32_t w = -1;
+    const int64_t sm = sum();
+    for (int32_t s = 0; s < S; ++s)
+      if (sm + g[s] <= G && (w < 0 || F[s] * g[w] > F[w] * g[s])) w = s;
+    g[w] *= 2;
+  }
+  return g;
+}
+
+// Reading R-10 (cost with per-stage GPU counts): plan p = k*nB + b runs every
+// stage with tp = 2^k (k <= log2 min g_s) and dp_s = g_s / tp; stage s is
+// costed with the §N5 terms at its own dp_s and mb_s = GB/(B dp_s) (as NEXT-1,
+// R-5).  GPUs are packed from a node boundary in stage order (offset o_s =
+// sum of the earlier g): tp groups are intra-node iff tp <= gpn and tp | o_s;
+// the dp all-reduce is intra iff the stage lies within one node; the boundary
+// into s is intra iff o_s is not a node boundary -- for uniform g these are
+// exactly A-15.  A Cell whose stages exceed g_max is infeasible.
+PlanOut paper_plan_cost(const oracle_problem *pr, int32_t j, int32_t t, int32_t S,
+                        const std::vector<int32_t> &b, const std::vector<int32_t> &g, int32_t p) {
+  const int64_t off = pr->layer_off[j];
+  const int64_t TL = pr->layer_off[pr->n_jobs];
+  const int32_t nB = n_bvalues(pr);
+  const int32_t k = p / nB;
+  const int32_t B = b_value(pr, S, p % nB);
+  const i128 tp = (i128)1 << k, GB = pr->gb[j];
+  const int64_t gpn = pr->gpn[t];
+  const int32_t *ck = pr->c + ((int64_t)t * (pr->k_max + 1) + k) * TL + off;
+  bool feasible = true;
+  i128 sumT = 0, maxT = 0, maxSync = 0;
+  int64_t o = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    if (g[s] > pr->g_max || (i128)g[s] < tp) return {false, 0};
+    const i128 dp = (i128)g[s] / tp;
+    if (B * dp > GB) return {false, 0};
+    const i128 mb = GB / (B * dp);
+    const bool tp_in = tp <= gpn && o % (int64_t)tp == 0;
+    const bool dp_in = o / gpn == (o + g[s] - 1) / gpn;
+    const i128 a_tp = tp_in ? pr->alpha_in[t] : pr->alpha_x[t];
+    const i128 b_tp = tp_in ? pr->beta_in[t] : pr->beta_x[t];
+    const i128 a_dp = dp_in ? pr->alpha_in[t] : pr->alpha_x[t];
+    const i128 b_dp = dp_in ? pr->beta_in[t] : pr->beta_x[t];
+    i128 C = 0, TPV = 0, TPN = 0, W = 0, A = 0;
+    for (int32_t l = b[s]; l < b[s + 1]; ++l) {
+      C += ck[l];
+      TPV += pr->tpv[off + l];
+      TPN += pr->tpn[off + l];
+      W += pr->w[off + l];
+      A += pr->act[off + l];
+    }
+    i128 inb = 0;
+    if (s > 0) {
+      const bool b_in = o % gpn != 0;
+      const i128 a_b = b_in ? pr->alpha_in[t] : pr->alpha_x[t];
+      const i128 b_b = b_in ? pr->beta_in[t] : pr->beta_x[t];
+      const i128 V = mb * pr->bnd[off + b[s] - 1];
+      inb = P2P(a_b, b_b, cdiv(V, tp)) + AG(tp, a_tp, b_tp, V);
+    }
+    const i128 T = mb * C + AR(tp, a_tp, b_tp, mb * TPV, TPN) + inb;
+    const i128 sync = AR(dp, a_dp, b_dp, cdiv(W, tp), 1);
+    const i128 mem = cdiv((i128)pr->kst[j] * W + (GB / dp) * A, tp);
+    if (mem > pr->mem[t]) feasible = false;
+    sumT += T;
+    maxT = std::max(maxT, T);
+    maxSync = std::max(maxSync, sync);
+    o += g[s];
+  }
+  return {feasible, narrow(sumT + (i128)(B - 1) * maxT + maxSync)};
+}
+
 bool valid_problem(const oracle_problem *pr) {
   if (!pr || pr->n_types < 1 || pr->n_jobs < 0 || pr->k_max < 0) return false;
   if (pr->s_max < 1 || pr->g_max < 1 || pr->g_max > (1 << pr->k_max) || pr->depth < 0) return false;
@@ -371,6 +537,94 @@ int oracle_estimate(const oracle_problem *pr, const int32_t *cell_job, const int
       plan[i - c0] = best_p;
     }
   } catch (Overflow &) {
+    return 7;
+  }
+  return 0;
+}
+
+// NEXT-2: cuts (bounds[S+1]) and per-stage GPU counts (g[S]) of (j, t, G, S).
+int oracle_paper_stages(const oracle_problem *pr, int32_t j, int32_t t, int32_t G, int32_t S,
+                        int32_t *bounds, int32_t *g) {
+  if (!valid_problem(pr) || j < 0 || j >= pr->n_jobs || S < 1 || S > pr->n_layers[j] || G < S)
+    return 2;
+  const std::vector<int32_t> b = paper_cuts(pr, j, t, S);
+  for (int32_t s = 0; s <= S; ++s) bounds[s] = b[s];
+  if (g) {
+    const std::vector<int32_t> gg = paper_gpus(pr, j, t, G, b);
+    for (int32_t s = 0; s < S; ++s) g[s] = gg[s];
+  }
+  return 0;
+}
+
+// NEXT-2 pieces for the pins: x = num/den rounded (R-9), and the fractional
+// GPUs G F_s / F of the stages of given bounds (num[s] over den).
+int32_t oracle_paper_round_pow2(int64_t num, int64_t den) { return round_pow2(num, den); }
+
+int oracle_paper_fractional(const oracle_problem *pr, int32_t j, int32_t t, int32_t G, int32_t S,
+                            const int32_t *bounds, int64_t *num, int64_t *den) {
+  if (!valid_problem(pr)) return 2;
+  const int64_t off = pr->layer_off[j];
+  const int64_t TL = pr->layer_off[pr->n_jobs];
+  const int32_t *c0 = pr->c + ((int64_t)t * (pr->k_max + 1) + 0) * TL + off;
+  i128 F = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    i128 Fs = 0;
+    for (int32_t l = bounds[s]; l < bounds[s + 1]; ++l) Fs += c0[l];
+    num[s] = narrow((i128)G * Fs);
+    F += Fs;
+  }
+  *den = narrow(F);
+  return 0;
+}
+
+// NEXT-2 plan cost of plan p given explicit bounds and per-stage GPU counts.
+int oracle_paper_plan_cost(const oracle_problem *pr, int32_t j, int32_t t, int32_t S,
+                           const int32_t *bounds, const int32_t *g, int32_t p, int64_t *t_iter,
+                           int32_t *feasible) {
+  if (!valid_problem(pr)) return 2;
+  try {
+    const PlanOut r = paper_plan_cost(pr, j, t, S, std::vector<int32_t>(bounds, bounds + S + 1),
+                                      std::vector<int32_t>(g, g + S), p);
+    *t_iter = r.feasible ? r.t_iter : INF;
+    *feasible = r.feasible;
+  } catch (const Overflow &) {
+    return 7;
+  }
+  return 0;
+}
+
+// NEXT-2 estimate for Cells [c0, c1): the paper's stages and GPU counts, then
+// the first-minimum plan over k <= log2 min g_s and every B (p = k*nB + b).
+// stage_lg[(i-c0)*kstride + s] = log2 g_s (-1 padding).
+int oracle_estimate_paper(const oracle_problem *pr, const int32_t *cell_job,
+                          const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                          int64_t c0, int64_t c1, int64_t *t_ns, int32_t *plan, int8_t *stage_lg,
+                          int32_t kstride) {
+  if (!valid_problem(pr)) return 2;
+  try {
+    for (int64_t i = c0; i < c1; ++i) {
+      const int32_t j = cell_job[i], t = cell_type[i], G = cell_G[i], S = cell_S[i];
+      const std::vector<int32_t> b = paper_cuts(pr, j, t, S);
+      const std::vector<int32_t> g = paper_gpus(pr, j, t, G, b);
+      int32_t gmin = g[0];
+      for (int32_t x : g) gmin = std::min(gmin, x);
+      int64_t best = INF;
+      int32_t bp = -1;
+      const int32_t np = (ilog2(gmin) + 1) * n_bvalues(pr);
+      for (int32_t p = 0; p < np; ++p) {
+        const PlanOut r = paper_plan_cost(pr, j, t, S, b, g, p);
+        if (r.feasible && r.t_iter < best) {
+          best = r.t_iter;
+          bp = p;
+        }
+      }
+      t_ns[i - c0] = best;
+      plan[i - c0] = bp;
+      if (stage_lg)
+        for (int32_t s = 0; s < kstride; ++s)
+          stage_lg[(i - c0) * kstride + s] = (int8_t)(s < S ? ilog2(g[s]) : -1);
+    }
+  } catch (const Overflow &) {
     return 7;
   }
   return 0;

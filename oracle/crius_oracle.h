@@ -82,6 +82,23 @@ int oracle_tune_assembled(const oracle_problem *pr, int32_t form, const int32_t 
                           int64_t c0, int64_t c1, const int8_t *favor, int32_t kstride,
                           int64_t *t_ns, int32_t *bidx, int8_t *stage_k);
 
+/* NEXT-2: the paper's stage determination:
+ * cuts at the S-1 smallest boundary bytes (ties: min-max tp=1 compute, R0),
+ * FLOP-proportional GPUs per stage rounded to powers of two with conservation
+ * repair, plans with uniform tp and per-stage dp (R-8..R-10). */
+int oracle_paper_stages(const oracle_problem *pr, int32_t j, int32_t t, int32_t G, int32_t S,
+                        int32_t *bounds, int32_t *g);
+int32_t oracle_paper_round_pow2(int64_t num, int64_t den);
+int oracle_paper_fractional(const oracle_problem *pr, int32_t j, int32_t t, int32_t G, int32_t S,
+                            const int32_t *bounds, int64_t *num, int64_t *den);
+int oracle_paper_plan_cost(const oracle_problem *pr, int32_t j, int32_t t, int32_t S,
+                           const int32_t *bounds, const int32_t *g, int32_t p, int64_t *t_iter,
+                           int32_t *feasible);
+int oracle_estimate_paper(const oracle_problem *pr, const int32_t *cell_job,
+                          const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                          int64_t c0, int64_t c1, int64_t *t_ns, int32_t *plan, int8_t *stage_lg,
+                          int32_t kstride);
+
 /* O5: the §N6 round over all Cells.  free_in may be NULL (= capacity).
  * decision[j] = Cell id | -1 pending | -2 unschedulable. */
 int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,
