@@ -196,6 +196,25 @@ crius_status crius_tune_assembled(crius_ctx *ctx, int32_t pipeline_form, int64_t
                                   int64_t unit_end, const int8_t *d_favor,
                                   crius_cell_result *d_out, int8_t *d_stage_tp, void *stream);
 
+/* NEXT-2: the paper's stage determination (PAPER.md:266-283,
+ * "Stage determination of a Cell"), readings R-8..R-10 of DESIGN.md §13.
+ * Per (job, type, S) the model is cut at the S-1 inter-layer gaps with the
+ * smallest boundary bytes; gaps tied at the (S-1)-th smallest byte
+ * count are chosen by the min-max of the tp=1 compute with the R0 rule.
+ * Per Cell, stage s gets G * F_s / F GPUs (F = tp=1 compute, the FLOP proxy;
+ * "T_elapsed = FLOPs / Number_GPU") rounded to the nearest power of
+ * two (ties up, >= 1) with a conservation repair to sum G.  Plans
+ * p = k * nB + b run tp = 2^k in every stage (k <= log2 min g_s) and
+ * dp_s = g_s / tp; GPUs are packed from a node boundary in stage order, which
+ * fixes the intra/inter link of every term.  A Cell with a stage above g_max
+ * is infeasible.  d_out[i] as crius_estimate_cells (t_ns, plan = p, flags);
+ * d_splits (optional DEVICE int16) receives the cuts in the split layout;
+ * d_stage_lg (optional DEVICE int8, rows of crius_max_stages entries) receives
+ * log2 g_s per stage, -1 padding.  Asynchronous on `stream`. */
+crius_status crius_estimate_paper_stages(crius_ctx *ctx, int64_t unit_begin, int64_t unit_end,
+                                         crius_cell_result *d_out, int16_t *d_splits,
+                                         int8_t *d_stage_lg, void *stream);
+
 /* Largest stage count S of the enumerated Cells (row length of d_stage_tp). */
 int32_t crius_max_stages(const crius_ctx *ctx);
 

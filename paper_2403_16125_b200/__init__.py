@@ -72,6 +72,7 @@ class _CellView(C.Structure):
 EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_enumerate_cells", "crius_cells",
            "crius_split_stride", "crius_max_stages", "crius_partition_units",
            "crius_estimate_cells", "crius_estimate_assembled", "crius_tune_assembled",
+           "crius_estimate_paper_stages",
            "crius_compact_gathered", "crius_schedule_round", "crius_schedule_round_state",
            "crius_round_stats",
            "crius_kernel_launches",
@@ -100,6 +101,7 @@ def lib():
         L.crius_estimate_cells.argtypes = [vp, i64, i64, vp, vp, vp]
         L.crius_estimate_assembled.argtypes = [vp, C.POINTER(_Assembly), i64, i64, vp, vp, vp]
         L.crius_tune_assembled.argtypes = [vp, i32, i64, i64, vp, vp, vp, vp]
+        L.crius_estimate_paper_stages.argtypes = [vp, i64, i64, vp, vp, vp, vp]
         L.crius_max_stages.argtypes = [vp]
         L.crius_max_stages.restype = i32
         L.crius_compact_gathered.argtypes = [vp, vp, i64, i32, vp, vp, vp]
@@ -260,6 +262,24 @@ class Crius:
         _check(lib().crius_estimate_assembled(self.ctx, C.byref(cfg), int(unit_begin),
                                               int(unit_end), C.c_void_p(out.data_ptr()), sp,
                                               _stream_handle(stream)))
+        return out
+
+    def estimate_paper_stages(self, unit_begin=0, unit_end=None, out=None, splits=None,
+                              stage_lg=None, stream=None):
+        """NEXT-2: the paper's stage determination (cuts at the smallest boundary
+        bytes, FLOP-proportional power-of-two GPUs per stage) and the best plan
+        (uniform tp, per-stage dp).  Records as estimate(); splits as estimate();
+        stage_lg: optional int8 [n_cells, max_stages] device tensor (log2 g_s)."""
+        if self.n_cells is None:
+            self.enumerate(stream)
+        unit_end = self.n_units if unit_end is None else unit_end
+        if out is None:
+            out = self.new_results(self.n_cells)
+        sp = C.c_void_p(splits.data_ptr()) if splits is not None else None
+        lg = C.c_void_p(stage_lg.data_ptr()) if stage_lg is not None else None
+        _check(lib().crius_estimate_paper_stages(self.ctx, int(unit_begin), int(unit_end),
+                                                 C.c_void_p(out.data_ptr()), sp, lg,
+                                                 _stream_handle(stream)))
         return out
 
     def tune_assembled(self, favor, form=1, unit_begin=0, unit_end=None, out=None, stage_tp=None,

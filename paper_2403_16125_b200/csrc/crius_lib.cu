@@ -634,8 +634,9 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   A.off_NRAW = take(Lp * 4);
   A.off_POFF = take(maxCells * 8);
   A.off_ORD = take((maxCells + 1) * 4);
-  A.st_cap = amode ? Stop * (amode == 1 ? 2 : K1e) : 0;  // modes 2, 3: every k
+  A.st_cap = (amode == 0 || amode == 4) ? 0 : Stop * (amode == 1 ? 2 : K1e);  // modes 2, 3: every k
   A.off_ST = take(A.st_cap * 25);
+  A.off_PS = take(amode == 4 ? Lp * 12 + Stop * 4 : 0);
   A.warp_bytes = o;
   const int64_t nunits = unit_end - unit_begin;
   CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
@@ -657,8 +658,10 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
     kern = warps == 4 ? k_estimate<4, 1, 1> : k_estimate<1, 1, 1>;
   else if (amode == 2)
     kern = warps == 4 ? k_estimate<4, 1, 2> : k_estimate<1, 1, 2>;
-  else
+  else if (amode == 3)
     kern = warps == 4 ? k_estimate<4, 1, 3> : k_estimate<1, 1, 3>;
+  else
+    kern = warps == 4 ? k_estimate<4, 1, 4> : k_estimate<1, 1, 4>;
   int per_sm = 1;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
@@ -691,6 +694,14 @@ crius_status crius_estimate_assembled(crius_ctx *c, const crius_assembly *asm_cf
     return fail(CRIUS_EINVAL, "pipeline_form must be 0 or 1");
   return launch_estimate(c, asm_cfg->mode, asm_cfg->pipeline_form, unit_begin, unit_end, d_out,
                          nullptr, d_stage_tp, nullptr, (cudaStream_t)stream);
+}
+
+crius_status crius_estimate_paper_stages(crius_ctx *c, int64_t unit_begin, int64_t unit_end,
+                                        crius_cell_result *d_out, int16_t *d_splits,
+                                        int8_t *d_stage_lg, void *stream) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  return launch_estimate(c, 4, 0, unit_begin, unit_end, d_out, d_splits, d_stage_lg, nullptr,
+                         (cudaStream_t)stream);
 }
 
 crius_status crius_tune_assembled(crius_ctx *c, int32_t pipeline_form, int64_t unit_begin,

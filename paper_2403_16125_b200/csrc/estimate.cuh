@@ -42,6 +42,7 @@ struct EstArgs {
   const int8_t *favor;     // AMODE 3 (tuner): [cell][stage_stride] log2 tp of the estimated plan
   int32_t stage_stride;
   int32_t off_ST, st_cap;  // per-warp stage table (st_cap entries)
+  int32_t off_PS;          // NEXT-2 scratch: sorted gap bytes [Lp] i64, LF [Lp] i32, g [Stop] i32
 };
 
 // Inclusive prefix of a profile row into dst[0..L] (dst[0] = 0).
@@ -402,6 +403,163 @@ __device__ void assembled_cell(const UnitCtx &U, const EstArgs &A, int G, int S,
   }
 }
 
+// ---- NEXT-2: the paper's stage determination ----------
+// Cuts (R-8): the S-1 gaps with the smallest boundary bytes; the gaps below the
+// (S-1)-th smallest byte count are forced, the rest are taken among the gaps
+// equal to it by the min-max of the tp=1 compute with the R0 rule.  One warp,
+// lanes over the end position i; f[s][i] = min over allowed k in
+// [max(s-1, LF(i)), i-1] of max(f[s-1][k], P[i]-P[k]) (LF(i) = last forced gap
+// below i: no forced gap may fall inside a stage), lowest k on ties.
+__device__ void paper_cuts_unit(const int64_t *P, const int64_t *BNDr, int L, int S, int Lp,
+                                const int64_t *SB, int32_t *LF, int64_t *F0, int64_t *F1,
+                                uint8_t *ARG, int16_t *bd, int lane) {
+  if (S == 1) {
+    if (lane == 0) {
+      bd[0] = 0;
+      bd[1] = (int16_t)L;
+    }
+    __syncwarp();
+    return;
+  }
+  const int64_t beta = SB[S - 2];
+  // gap q in [1, L-1] carries BNDr[q-1]; allowed = bytes <= beta, forced = bytes < beta
+  for (int i = lane; i <= L; i += 32) {
+    int lf = 0;
+    for (int q = i - 1; q >= 1; --q)
+      if (BNDr[q - 1] < beta) {
+        lf = q;
+        break;
+      }
+    LF[i] = lf;
+    const bool end_ok = i == L || (i >= 1 && BNDr[i - 1] <= beta);
+    F0[i] = (i >= 1 && end_ok && lf == 0) ? P[i] : kInf;
+  }
+  __syncwarp();
+  int64_t *fp = F0, *fc = F1;
+  for (int s = 2; s <= S; ++s) {
+    uint8_t *arow = ARG + s * Lp;
+    for (int i = lane; i <= L; i += 32) {
+      int64_t best = kInf;
+      int a = 0;
+      const bool end_ok = i == L || (i >= 1 && BNDr[i - 1] <= beta);
+      if (end_ok && i >= s) {
+        const int64_t Pi = P[i];
+        for (int k = max(s - 1, LF[i]); k <= i - 1; ++k) {
+          if (BNDr[k - 1] > beta || fp[k] == kInf) continue;
+          const int64_t v = max(fp[k], Pi - P[k]);
+          if (v < best) {
+            best = v;
+            a = k;
+          }
+        }
+      }
+      fc[i] = best;
+      arow[i] = (uint8_t)a;
+    }
+    __syncwarp();
+    int64_t *tmp = fp;
+    fp = fc;
+    fc = tmp;
+  }
+  if (lane == 0) {
+    bd[S] = (int16_t)L;
+    int b = L;
+    for (int s = S; s >= 2; --s) {
+      b = ARG[s * Lp + b];
+      bd[s - 1] = (int16_t)b;
+    }
+    bd[0] = 0;
+  }
+  __syncwarp();
+}
+
+// GPUs per stage (R-9): round(G F_s / F) to the nearest power of two (ties up,
+// >= 1), then conservation repair (halve the lowest F_s/g_s among g_s >= 2
+// while the sum exceeds G; double the highest F_s/g_s that keeps the sum <= G
+// while it is below).  One lane; 128-bit products.
+__device__ void paper_gpus_lane(const int64_t *P, const int16_t *bd, int S, int G, int32_t *g) {
+  const __int128 F = P[bd[S]] - P[bd[0]];
+  int64_t sum = 0;
+  for (int s = 0; s < S; ++s) {
+    const __int128 num = (__int128)G * (P[bd[s + 1]] - P[bd[s]]);
+    int v = 1;
+    if (num >= F) {
+      int a = 0;
+      while (((__int128)2 << a) * F <= num) ++a;
+      v = (2 * num >= 3 * ((__int128)1 << a) * F) ? (2 << a) : (1 << a);
+    }
+    g[s] = v;
+    sum += v;
+  }
+  while (sum > G) {
+    int w = -1;
+    for (int s = 0; s < S; ++s) {
+      if (g[s] < 2) continue;
+      if (w < 0 || (__int128)(P[bd[s + 1]] - P[bd[s]]) * g[w] < (__int128)(P[bd[w + 1]] - P[bd[w]]) * g[s])
+        w = s;
+    }
+    sum -= g[w] / 2;
+    g[w] /= 2;
+  }
+  while (sum < G) {
+    int w = -1;
+    for (int s = 0; s < S; ++s) {
+      if (sum + g[s] > G) continue;
+      if (w < 0 || (__int128)(P[bd[s + 1]] - P[bd[s]]) * g[w] > (__int128)(P[bd[w + 1]] - P[bd[w]]) * g[s])
+        w = s;
+    }
+    sum += g[w];
+    g[w] *= 2;
+  }
+}
+
+// T_iter of plan (k, lB) over stages with GPU counts g (R-10): uniform tp = 2^k,
+// dp_s = g_s / tp, mb_s = GB/(B dp_s); GPUs packed from a node boundary in
+// stage order (offset o): tp intra iff tp <= gpn and tp | o; dp intra iff the
+// stage lies in one node; boundary into s intra iff o is not a node boundary.
+__device__ __forceinline__ int64_t paper_plan_time(const UnitCtx &U, const int16_t *bd,
+                                                   const int32_t *g, int S, int k, int lB,
+                                                   int gpn) {
+  const uint64_t tp = 1ull << k;
+  int64_t sumT = 0, maxT = 0, maxSync = 0;
+  int64_t o = 0;
+  const int64_t *PCk = U.PC + k * U.Lp;
+  for (int s = 0; s < S; ++s) {
+    const int gs = g[s], a = bd[s], e = bd[s + 1];
+    const int ldp = ilog2_pow2((uint32_t)gs) - k;
+    if (ldp < 0 || lB + ldp > U.lGB) return kInf;  // tp <= g_s; B dp <= GB (A-12)
+    const int lmb = U.lGB - lB - ldp;
+    const uint64_t dp = 1ull << ldp;
+    const bool tp_in = (int64_t)tp <= gpn && (o & (int64_t)(tp - 1)) == 0;
+    const bool dp_in = o / gpn == (o + gs - 1) / gpn;
+    const uint64_t a_tp = tp_in ? U.a_in : U.a_x, b_tp = tp_in ? U.b_in : U.b_x;
+    const uint64_t a_dp = dp_in ? U.a_in : U.a_x, b_dp = dp_in ? U.b_in : U.b_x;
+    const int64_t W = U.PW[e] - U.PW[a], A = U.PA[e] - U.PA[a];
+    const uint64_t mem = ((uint64_t)(U.kst * W + (A << (U.lGB - ldp))) + tp - 1) >> k;
+    if (mem > (uint64_t)U.memt) return kInf;
+    uint64_t T = (uint64_t)(PCk[e] - PCk[a]) << lmb;
+    if (k) {
+      const uint64_t V = (uint64_t)(U.PV[e] - U.PV[a]) << lmb;
+      T += (uint64_t)(U.PN[e] - U.PN[a]) * (2 * (tp - 1)) * a_tp + mul_shr_ceil(2 * (tp - 1) * V, b_tp, k + 20);
+    }
+    if (s) {
+      const uint64_t Vb = (uint64_t)U.BND[a - 1] << lmb;
+      const bool b_in = o % gpn != 0;
+      T += (b_in ? U.a_in : U.a_x) + mul_shr_ceil((Vb + tp - 1) >> k, b_in ? U.b_in : U.b_x, 20);
+      if (k) T += (tp - 1) * a_tp + mul_shr_ceil((tp - 1) * Vb, b_tp, k + 20);
+    }
+    if (ldp) {
+      const uint64_t Wt = ((uint64_t)W + tp - 1) >> k;
+      const uint64_t sy = 2 * (dp - 1) * a_dp + mul_shr_ceil(2 * (dp - 1) * Wt, b_dp, ldp + 20);
+      maxSync = max(maxSync, (int64_t)sy);
+    }
+    sumT += (int64_t)T;
+    maxT = max(maxT, (int64_t)T);
+    o += gs;
+  }
+  return sumT + (int64_t)((1ll << lB) - 1) * maxT + maxSync;
+}
+
 // ---- cp.async (LDGSTS) staging: global -> shared without registers ---------
 __device__ __forceinline__ void cp_async4(void *sdst, const void *gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
@@ -532,6 +690,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned char *base = smem + (size_t)wid * A.warp_bytes;
+  const int Lp_ = A.Lp;
   int64_t *PC = (int64_t *)(base + A.off_PC);
   int64_t *PW = (int64_t *)(base + A.off_PW);
   int64_t *PA = (int64_t *)(base + A.off_PA);
@@ -550,6 +709,9 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
   int64_t *STT = (int64_t *)(base + A.off_ST);     // [st_cap] stage table (AMODE > 0)
   int64_t *STC = STT + A.st_cap, *STY = STC + A.st_cap;
   uint8_t *STOK = (uint8_t *)(STY + A.st_cap);
+  int64_t *PSB = (int64_t *)(base + A.off_PS);     // NEXT-2: sorted gap bytes [Lp]
+  int32_t *PLF = (int32_t *)(PSB + Lp_);           // NEXT-2: last forced gap [Lp]
+  int32_t *PGS = PLF + Lp_;                        // NEXT-2: GPUs per stage [Stop]
   const int Lp = A.Lp;
   const int64_t out_cell_base = A.ucb[A.unit_begin];
 
@@ -623,6 +785,21 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
     warp_prefix32(PN, NRAW, L, lane);
     __syncwarp();
 
+    const int nSi = ilog2_pow2(smax) + 1;
+    if (AMODE == 4) {  // NEXT-2: the paper's cuts for every S of the unit
+      // gap bytes sorted ascending (rank by counting; index breaks ties)
+      for (int q = lane; q < L - 1; q += 32) {
+        const int64_t v = BND[q];
+        int r = 0;
+        for (int q2 = 0; q2 < L - 1; ++q2) r += BND[q2] < v || (BND[q2] == v && q2 < q);
+        PSB[r] = v;
+      }
+      __syncwarp();
+      for (int si = 0; si < nSi; ++si) {
+        const int S = 1 << si;
+        paper_cuts_unit(PC, BND, L, S, Lp, PSB, PLF, F0, F1, ARG, BD + (S - 1) + si, lane);
+      }
+    } else {
     // ---- K2: stage DP rows f[1..smax] over P0 = PC[0]
     if (PC[L] < (int64_t)INT32_MAX) {
       int32_t *P32 = NRAW;
@@ -634,7 +811,6 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
     }
 
     // ---- R0 backtrack, one lane per S = 2^si
-    const int nSi = ilog2_pow2(smax) + 1;
     if (lane < nSi) {
       const int S = 1 << lane;
       int16_t *bd = BD + (S - 1) + lane;
@@ -647,6 +823,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
       }
       bd[0] = 0;
     }
+    }  // AMODE != 4
     __syncwarp();
     if (split_out) {
       const int used = (1 << nSi) - 1 + nSi;
@@ -675,6 +852,52 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
     U.b_x = P.ty[t].b_x;
     U.lBv = P.lB;
 
+    if (AMODE == 4) {  // NEXT-2: per Cell, the paper's GPUs per stage, then every (k, B)
+      const int gpn = P.ty[t].gpn;
+      const int nB = P.b_mode == 0 ? 1 : P.nB;
+      for (int ci = 0; ci < nc; ++ci) {
+        const int G = CG[ci], S = CS[ci], lS = ilog2_pow2(S);
+        const int16_t *bd = BD + (S - 1) + lS;
+        if (lane == 0) paper_gpus_lane(PC, bd, S, G, PGS);
+        __syncwarp();
+        int gmin = INT32_MAX, gmx = 0;
+        for (int s = lane; s < S; s += 32) {
+          gmin = min(gmin, PGS[s]);
+          gmx = max(gmx, PGS[s]);
+        }
+        gmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)gmin);
+        gmx = warp_max_int(gmx);
+        const int nitem = gmx > P.g_max ? 0 : (ilog2_pow2((uint32_t)gmin) + 1) * nB;
+        int64_t bT = kInf;
+        int bp = INT32_MAX;
+        for (int it = lane; it < nitem; it += 32) {
+          const int k = it / nB, bi = it - k * nB;
+          const int lB = P.b_mode == 0 ? lS + 2 : P.lB[bi];
+          const int64_t T = paper_plan_time(U, bd, PGS, S, k, lB, gpn);
+          if (T < bT) {  // items ascending per lane: ties keep the lower p
+            bT = T;
+            bp = it;
+          }
+        }
+        int64_t wT = bT;
+        for (int d = 16; d > 0; d >>= 1) wT = min(wT, __shfl_xor_sync(0xffffffffu, wT, d));
+        const int wp = (int)__reduce_min_sync(0xffffffffu, (unsigned)(bT == wT ? bp : INT32_MAX));
+        int8_t *kout = A.stage_tp ? A.stage_tp + (cb + ci - out_cell_base) * A.stage_stride : nullptr;
+        if (kout)
+          for (int q = lane; q < A.stage_stride; q += 32)
+            kout[q] = (int8_t)(q < S ? ilog2_pow2((uint32_t)PGS[q]) : -1);
+        if (lane == 0) {
+          CellResult res;
+          const bool ok = wT != kInf;
+          res.t_ns = ok ? wT : kInf;
+          res.plan = ok ? wp : -1;
+          res.flags = ok ? 1 : 0;
+          A.out[cb + ci - out_cell_base] = res;
+        }
+        __syncwarp();
+      }
+      continue;
+    }
     if (AMODE > 0) {  // NEXT-1: per-stage assembly, one Cell at a time
       for (int ci = 0; ci < nc; ++ci) {
         int64_t F;
