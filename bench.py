@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--form", type=int, default=1, help="pipeline form for --assembly (1 = paper)")
     ap.add_argument("--tune", action="store_true",
                     help="NEXT-3: after --assembly 1, tune every Cell in its favoured halves")
+    ap.add_argument("--paper-stages", action="store_true",
+                    help="NEXT-2: the paper's stage determination instead of the min-max DP")
     return ap.parse_args()
 
 
@@ -64,6 +66,7 @@ def workload_name(a):
     s = f"x{a.scale}" if a.scale != 1 else ""
     m = f"-assembly{a.assembly}form{a.form}" if getattr(a, "assembly", 0) else ""
     m += "-tuned" if getattr(a, "tune", False) else ""
+    m += "-paperstages" if getattr(a, "paper_stages", False) else ""
     return f"cfg{a.config}{v}{s}{m}"
 
 
@@ -298,7 +301,9 @@ def main():
         if world > 1:
             sharded.ShardPlan(cr, world)  # partition is part of the step (a tiny kernel + D2H)
         e1.record(stream)
-        if a.assembly:
+        if a.paper_stages:
+            cr.estimate_paper_stages(int(ub[rank]), int(ub[rank + 1]), out=mine)
+        elif a.assembly:
             cr.estimate_assembled(a.assembly, a.form, int(ub[rank]), int(ub[rank + 1]), out=mine,
                                   stage_tp=stage_tp)
             if a.tune:
