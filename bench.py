@@ -238,7 +238,7 @@ def _par_estimate(rng):
 
 def cpu_parallel(pr, cells, c1):
     """the oracle's estimation of Cells [0, c1) sharded over P =
-    os.cpu_count() forked processes by contiguous work-balanced Cell ranges
+    (usable host cores) forked processes by contiguous work-balanced Cell ranges
     (weight nplans * S); the round stays single-threaded."""
     import multiprocessing as mp
     P = max(1, len(os.sched_getaffinity(0)))
