@@ -803,7 +803,6 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   R.free_io = c->d_free;
   R.total = c->d_total;
   R.stats = c->d_round_stats;
-  R.list = c->d_list;
   R.run_cell = run_cell ? c->d_run_cell : nullptr;
   R.active = active ? c->d_active : nullptr;
   R.run_opt = c->d_run_opt;
@@ -858,6 +857,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
     CK(dalloc(&c->eg.t2, J));
   }
   R.eg = c->eg;
+  R.list = c->d_list;  // allocated above (global-record mode only)
   CK(cudaFuncSetAttribute(k_round_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   k_round_greedy<<<1, kRoundThreads, dsm, st>>>(R, adm_in_smem, c->adm_glob, win_cap);
   CKL();

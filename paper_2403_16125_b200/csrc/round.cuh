@@ -152,7 +152,10 @@ __device__ __forceinline__ bool kappa_less(const OptRec &a, const OptRec &b) {
 constexpr int kRoundThreads = 1024;
 constexpr int kRT = 8;  // GPU types supported by the round kernel (shared-memory tables)
 constexpr int kRoundWarps = kRoundThreads / 32;
-constexpr int kAdmSmem = 2048;  // admitted-job records kept in shared memory up to this many
+#ifndef CRIUS_ADM_SMEM
+#define CRIUS_ADM_SMEM 2048
+#endif
+constexpr int kAdmSmem = CRIUS_ADM_SMEM;  // admitted-job records kept in shared memory up to this many
 constexpr int kAdmBytes = 76;   // bytes per admitted-job record (incl. scratch list)
 
 // Other-type options of the listed jobs, staged in shared memory by the warp

@@ -3,7 +3,8 @@
 k_round_greedy keeps the other-type move caches of the listed jobs in shared
 memory up to kECap entries (global memory beyond) and stages their options in
 a pool of kPool records (refills re-read global memory when a job got no
-room); the per-type move loops run on CRIUS_SEQ_WARPS warps.  The default
+room); the per-type move loops run on CRIUS_SEQ_WARPS warps; the admitted-job
+records live in shared memory up to kAdmSmem jobs (global memory beyond).  The default
 build hits the fast paths on most recomputations, so this test rebuilds the
 library with tiny capacities (every fallback taken) and with one warp per type,
 runs full rounds in a child process (CRIUS_LIB selects the variant) and
@@ -24,6 +25,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "caps_tiny.so": ["CRIUS_ECAP=4", "CRIUS_POOL=16", "CRIUS_SEQ_WARPS=1"],
     "caps_nopool.so": ["CRIUS_POOL=1", "CRIUS_SEQ_WARPS=2"],
+    "adm_global.so": ["CRIUS_ADM_SMEM=16", "CRIUS_SEQ_WARPS=8"],
 }
 
 CHILD = r"""
