@@ -7,6 +7,8 @@ timeout 300 python bench.py --steps 20 --warmup 3 > ${P}_bench4.json 2> ${P}_ben
 timeout 300 python bench.py --config 5 --steps 10 --warmup 3 --no-cpu-baseline > ${P}_bench5.json 2> ${P}_bench5.err
 timeout 300 python bench.py --config 4 --variant pow2 --steps 10 --warmup 3 --no-cpu-baseline > ${P}_bench4p.json 2> ${P}_bench4p.err
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > ${P}_ref4.json 2> ${P}_ref4.err
+timeout 300 python bench.py --paper-stages --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > ${P}_bench4ps.json 2> ${P}_bench4ps.err
+timeout 300 python bench.py --config 5 --paper-stages --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > ${P}_bench5ps.json 2> ${P}_bench5ps.err
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-flush"
 timeout 200 $CMD > ${P}_plain.log 2>&1 && \
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${P}_launches.csv $CMD > ${P}_ncu1.log 2>&1
