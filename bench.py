@@ -411,17 +411,28 @@ def main():
             tt = torch.from_numpy(arr).pin_memory()
             pin[k] = tt
             setattr(pr, k, tt.numpy())
-        h2d = sum(int(t.numel() * t.element_size()) for t in pin.values())
+        # a rank uploads the per-job arrays and the per-layer rows of its own jobs
+        # (SURVEY §8(e)); the partition depends on the per-job arrays only, which
+        # do not change between steps here, so the setup plan's job range holds
+        j0, j1 = plan.job_range(rank, pr.n_types) if world > 1 else (0, pr.n_jobs)
+        row_keys = ("c", "w", "act", "bnd", "tpv", "tpn")
+        l0, l1 = int(pr.layer_off[j0]), int(pr.layer_off[j1])
+        h2d = sum(int(t.numel() * t.element_size()) for k, t in pin.items() if k not in row_keys)
+        h2d += sum(int(pin[k].element_size()) * (int(pin[k].numel()) // pr.total_layers) * (l1 - l0)
+                   for k in row_keys)
         d2h = pr.n_jobs * 8 + pr.n_types * 4 + 8 + 3 * 8 + (pr.n_jobs + 1) * 4
 
         def e2e_step():
             # the user's call sequence: new profiles from host memory -> decisions on host
-            cr.update(pr)
-            cr.enumerate()
             if world > 1:
+                cr.update(pr, j0, j1)
+                cr.enumerate()
                 pl = sharded.ShardPlan(cr, world)
+                assert pl.job_range(rank, pr.n_types) == (j0, j1)
                 res = sharded.estimate_all(cr, pl, rank, mine=mine, gathered=gathered, full=full)
             else:
+                cr.update(pr)
+                cr.enumerate()
                 res = cr.estimate(out=mine)
             return cr.schedule_round(res)
 
@@ -440,8 +451,12 @@ def main():
         if world > 1:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
         e2e_ms = float(e2e_t.item())
+        bytes_t = torch.tensor([h2d, d2h], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(bytes_t)  # whole-job bytes: every rank's copies
         e2e = {"value": n_plans / (e2e_ms / 1e3), "unit": "cell-plans/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+               "h2d_bytes_per_step": int(bytes_t[0]), "d2h_bytes_per_step": int(bytes_t[1]),
+               "ms_per_step": e2e_ms}
 
     line = {"metric": "Cell-plan evaluations/sec", "value": value, "unit": "cell-plans/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,

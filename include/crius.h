@@ -128,6 +128,19 @@ crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cluster,
 crius_status crius_update_profiles(crius_ctx *ctx, const crius_cluster *cluster,
                                    const crius_jobs *jobs, void *stream);
 
+/* As crius_update_profiles, but the per-layer rows (compute_ns of every
+ * (type, k) plane, param/act/boundary/tp bytes, tp_calls) are copied and
+ * bound-checked only for jobs [job_begin, job_end); the per-job arrays and
+ * the cluster parameters are copied for every job.  A rank of a sharded run
+ * ("each rank needs H2D only for its jobs' profile rows") uploads
+ * the jobs of its unit range (crius_partition_units, units = (job, type) in job
+ * order) and must then estimate only Cells of those jobs; rows of the other
+ * jobs keep whatever values they had.  [0, n_jobs) == crius_update_profiles.
+ * EINVAL on a range outside [0, n_jobs]. */
+crius_status crius_update_profiles_range(crius_ctx *ctx, const crius_cluster *cluster,
+                                         const crius_jobs *jobs, int32_t job_begin,
+                                         int32_t job_end, void *stream);
+
 /* Enumerate every Cell (§N2) on the device: per-unit counts, scan,
  * fill.  Synchronises `stream` and returns the counts.  EINFEASIBLE if 0 Cells. */
 crius_status crius_enumerate_cells(crius_ctx *ctx, int64_t *n_cells, int64_t *n_cell_plans,

@@ -69,7 +69,8 @@ class _CellView(C.Structure):
                 ("unit_plan_begin", C.c_void_p)]
 
 
-EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_enumerate_cells", "crius_cells",
+EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_update_profiles_range",
+           "crius_enumerate_cells", "crius_cells",
            "crius_split_stride", "crius_max_stages", "crius_partition_units",
            "crius_estimate_cells", "crius_estimate_assembled", "crius_tune_assembled",
            "crius_estimate_paper_stages",
@@ -93,6 +94,8 @@ def lib():
         L.crius_load_profiles.argtypes = [C.POINTER(vp), C.POINTER(_Cluster), C.POINTER(_Jobs),
                                           C.POINTER(_Config), i32, vp]
         L.crius_update_profiles.argtypes = [vp, C.POINTER(_Cluster), C.POINTER(_Jobs), vp]
+        L.crius_update_profiles_range.argtypes = [vp, C.POINTER(_Cluster), C.POINTER(_Jobs), i32,
+                                                  i32, vp]
         L.crius_enumerate_cells.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), vp]
         L.crius_cells.argtypes = [vp, C.POINTER(_CellView)]
         L.crius_split_stride.argtypes = [vp]
@@ -187,10 +190,17 @@ class Crius:
         return cl, jb, cf
 
     # -- the C-ABI calls ------------------------------------------------------
-    def update(self, pr, stream=None):
+    def update(self, pr, job_begin=None, job_end=None, stream=None):
+        """New profile values (same shapes); per-layer rows only for jobs
+        [job_begin, job_end) when a range is given (a rank's shard)."""
         cl, jb, _ = self._structs(pr)
-        _check(lib().crius_update_profiles(self.ctx, C.byref(cl), C.byref(jb),
-                                           _stream_handle(stream)))
+        if job_begin is None:
+            _check(lib().crius_update_profiles(self.ctx, C.byref(cl), C.byref(jb),
+                                               _stream_handle(stream)))
+        else:
+            _check(lib().crius_update_profiles_range(self.ctx, C.byref(cl), C.byref(jb),
+                                                     int(job_begin), int(job_end),
+                                                     _stream_handle(stream)))
         self.pr = pr
 
     def enumerate(self, stream=None):

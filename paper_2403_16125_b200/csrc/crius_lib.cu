@@ -151,16 +151,16 @@ crius_status validate_static(const crius_cluster *cl, const crius_jobs *jb, cons
   if (jb->layer_off[0] != 0) return fail(CRIUS_EINVAL, "layer_off[0] must be 0");
   int32_t Lmax = 0;
   for (int j = 0; j < jb->n_jobs; ++j) {
-    const std::string js = "job " + std::to_string(j);
+    auto js = [j] { return "job " + std::to_string(j); };  // built only on failure
     if (!pow2(jb->n_gpus_req[j]) || jb->n_gpus_req[j] > (1 << 29))
-      return fail(CRIUS_EINVAL, js + ": N_G must be a power of two");
+      return fail(CRIUS_EINVAL, js() + ": N_G must be a power of two");
     if (!pow2(jb->global_batch[j]) || jb->global_batch[j] > (1 << 30))
-      return fail(CRIUS_EINVAL, js + ": global batch must be a power of two");
-    if (jb->k_state[j] < 1) return fail(CRIUS_EINVAL, js + ": k_state must be >= 1");
+      return fail(CRIUS_EINVAL, js() + ": global batch must be a power of two");
+    if (jb->k_state[j] < 1) return fail(CRIUS_EINVAL, js() + ": k_state must be >= 1");
     if (jb->n_layers[j] < 1 || jb->n_layers[j] > 255)
-      return fail(CRIUS_EINVAL, js + ": n_layers must be 1..255");
+      return fail(CRIUS_EINVAL, js() + ": n_layers must be 1..255");
     if (jb->layer_off[j + 1] != jb->layer_off[j] + jb->n_layers[j])
-      return fail(CRIUS_EINVAL, js + ": layer_off is not the prefix of n_layers");
+      return fail(CRIUS_EINVAL, js() + ": layer_off is not the prefix of n_layers");
     Lmax = std::max(Lmax, jb->n_layers[j]);
   }
   if (!(cf->gpu_set == 0 || cf->gpu_set == 1)) return fail(CRIUS_EINVAL, "gpu_set must be 0 or 1");
@@ -186,7 +186,7 @@ crius_status validate_static(const crius_cluster *cl, const crius_jobs *jb, cons
 
 // §N0 bounds with the per-job max of c measured on the device.
 crius_status validate_bounds(const crius_cluster *cl, const crius_jobs *jb, const crius_config *cf,
-                             const std::vector<int32_t> &maxc, int32_t minc) {
+                             const std::vector<int32_t> &maxc, int32_t minc, int j0, int j1) {
   typedef __int128 i128;
   if (minc < 1) return fail(CRIUS_EINVAL, "compute_ns must be >= 1 everywhere");
   const i128 LIM52 = (i128)1 << 52, LIM62 = (i128)1 << 62, LIM63 = (i128)1 << 63, MIB = 1 << 20;
@@ -196,8 +196,8 @@ crius_status validate_bounds(const crius_cluster *cl, const crius_jobs *jb, cons
     bmax = std::max<i128>(bmax, std::max(cl->beta_intra_ns_per_mib[t], cl->beta_inter_ns_per_mib[t]));
   }
   const i128 p = cf->g_max;  // tp, dp <= g <= g_max
-  for (int j = 0; j < jb->n_jobs; ++j) {
-    const std::string js = "job " + std::to_string(j);
+  for (int j = j0; j < j1; ++j) {
+    auto js = [j] { return "job " + std::to_string(j); };
     const int64_t o = jb->layer_off[j];
     const i128 L = jb->n_layers[j], GB = jb->global_batch[j];
     i128 W = 0, A = 0, V = 0, N = 0, Bm = 0;
@@ -206,18 +206,18 @@ crius_status validate_bounds(const crius_cluster *cl, const crius_jobs *jb, cons
       const int64_t bd = jb->boundary_bytes[o + l], tv = jb->tp_bytes[o + l];
       const int32_t tn = jb->tp_calls[o + l];
       if (w < 0 || a < 0 || bd < 0 || tv < 0 || tn < 0)
-        return fail(CRIUS_EINVAL, js + ": negative per-layer value");
+        return fail(CRIUS_EINVAL, js() + ": negative per-layer value");
       W += w;
       A += a;
       V += tv;
       N += tn;
       Bm = std::max<i128>(Bm, bd);
     }
-    if (L * maxc[j] * GB >= LIM52) return fail(CRIUS_EINVAL, js + ": L*max(c)*GB >= 2^52");
+    if (L * maxc[j] * GB >= LIM52) return fail(CRIUS_EINVAL, js() + ": L*max(c)*GB >= 2^52");
     if (2 * (p - 1) * GB * V >= LIM63 || p * GB * Bm >= LIM63 || 2 * (p - 1) * W >= LIM63)
-      return fail(CRIUS_EINVAL, js + ": alpha-beta numerator >= 2^63");
+      return fail(CRIUS_EINVAL, js() + ": alpha-beta numerator >= 2^63");
     if ((i128)jb->k_state[j] * W + GB * A >= LIM62)
-      return fail(CRIUS_EINVAL, js + ": kst*sum(w) + GB*sum(act) >= 2^62");
+      return fail(CRIUS_EINVAL, js() + ": kst*sum(w) + GB*sum(act) >= 2^62");
     const i128 comp = GB * L * maxc[j];
     const i128 tpc = N * 2 * (p - 1) * amax + L * (2 * (p - 1) * GB * V * bmax / MIB + 1);
     const i128 inb = L * (amax + GB * Bm * bmax / MIB + 1 + (p - 1) * amax + (p - 1) * GB * Bm * bmax / MIB + 1);
@@ -225,13 +225,13 @@ crius_status validate_bounds(const crius_cluster *cl, const crius_jobs *jb, cons
     const i128 sync = 2 * (p - 1) * amax + 2 * (p - 1) * W * bmax / MIB + 1;
     i128 Bmax = 4 * std::min<i128>(L, cf->s_max);
     if (cf->b_mode == 1) Bmax = cf->b_values[cf->b_count - 1];
-    if (Bmax * X + sync >= LIM62) return fail(CRIUS_EINVAL, js + ": T_iter bound >= 2^62");
+    if (Bmax * X + sync >= LIM62) return fail(CRIUS_EINVAL, js() + ": T_iter bound >= 2^62");
   }
   return CRIUS_OK;
 }
 
 crius_status copy_inputs(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
-                         cudaStream_t st) {
+                         cudaStream_t st, int j0, int j1) {
   const int J = jb->n_jobs, T = cl->n_types;
   const size_t TL = (size_t)c->TL;
   CK(cudaMemcpyAsync(c->d_ng, jb->n_gpus_req, J * 4, cudaMemcpyHostToDevice, st));
@@ -241,13 +241,21 @@ crius_status copy_inputs(crius_ctx *c, const crius_cluster *cl, const crius_jobs
   CK(cudaMemcpyAsync(c->d_off, jb->layer_off, (J + 1) * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->d_submit, jb->submit_time, J * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->d_id, jb->job_id, J * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->d_c, jb->compute_ns, (size_t)T * (jb->k_max + 1) * TL * 4,
-                     cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->d_w, jb->param_bytes, TL * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->d_act, jb->act_bytes, TL * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->d_bnd, jb->boundary_bytes, TL * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->d_tpv, jb->tp_bytes, TL * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->d_tpn, jb->tp_calls, TL * 4, cudaMemcpyHostToDevice, st));
+  if (j1 <= j0) return CRIUS_OK;
+  // per-layer rows of jobs [j0, j1): layers [l0, l1), one strided 2-D copy for c
+  const size_t l0 = (size_t)jb->layer_off[j0], nl = (size_t)jb->layer_off[j1] - l0;
+  const size_t planes = (size_t)T * (jb->k_max + 1);
+  if (nl == TL) {
+    CK(cudaMemcpyAsync(c->d_c, jb->compute_ns, planes * TL * 4, cudaMemcpyHostToDevice, st));
+  } else {
+    CK(cudaMemcpy2DAsync(c->d_c + l0, TL * 4, jb->compute_ns + l0, TL * 4, nl * 4, planes,
+                         cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemcpyAsync(c->d_w + l0, jb->param_bytes + l0, nl * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_act + l0, jb->act_bytes + l0, nl * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_bnd + l0, jb->boundary_bytes + l0, nl * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_tpv + l0, jb->tp_bytes + l0, nl * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_tpn + l0, jb->tp_calls + l0, nl * 4, cudaMemcpyHostToDevice, st));
   return CRIUS_OK;
 }
 
@@ -268,13 +276,15 @@ void fill_types(crius_ctx *c, const crius_cluster *cl) {
 
 // Device stats of c -> §N0 bounds; then priority ranks.  Synchronises.
 crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
-                         const crius_config *cf, cudaStream_t st) {
+                         const crius_config *cf, cudaStream_t st, int j0, int j1) {
   const int J = jb->n_jobs;
   CK(cudaMemsetAsync(c->d_scratch, 0, (J + 8) * 4, st));
   int32_t big = INT32_MAX;
   CK(cudaMemcpyAsync(c->d_scratch + J, &big, 4, cudaMemcpyHostToDevice, st));
-  k_profile_stats<<<J, 64, 0, st>>>(c->P, c->d_scratch, c->d_scratch + J);
-  CKL();
+  if (j1 > j0) {
+    k_profile_stats<<<j1 - j0, 64, 0, st>>>(c->P, j0, c->d_scratch, c->d_scratch + J);
+    CKL();
+  }
   CK(cudaMemsetAsync(c->d_rank, 0, (size_t)J * 4, st));
   const unsigned tiles = (unsigned)((J + 255) / 256);
   k_priority_count<<<dim3(tiles, tiles), 256, 0, st>>>(c->d_submit, c->d_id, J, c->d_rank);
@@ -286,7 +296,7 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
   CK(cudaMemcpyAsync(stats.data(), c->d_scratch, (J + 1) * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   std::vector<int32_t> maxc(stats.begin(), stats.begin() + J);
-  return validate_bounds(cl, jb, cf, maxc, stats[J]);
+  return validate_bounds(cl, jb, cf, maxc, j1 > j0 ? stats[J] : 1, j0, j1);
 }
 
 }  // namespace
@@ -385,9 +395,9 @@ crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cl, const
   P.bnd = c->d_bnd;
   P.tpv = c->d_tpv;
   P.tpn = c->d_tpn;
-  s = copy_inputs(c, cl, jb, st);
+  s = copy_inputs(c, cl, jb, st, 0, jb->n_jobs);
   if (s != CRIUS_OK) return cleanup(s);
-  s = finish_load(c, cl, jb, cf, st);
+  s = finish_load(c, cl, jb, cf, st, 0, jb->n_jobs);
   if (s != CRIUS_OK) return cleanup(s);
 #undef CKA
   *out = c;
@@ -397,6 +407,15 @@ crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cl, const
 crius_status crius_update_profiles(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
                                    void *stream) {
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  return crius_update_profiles_range(c, cl, jb, 0, c->P.J, stream);
+}
+
+crius_status crius_update_profiles_range(crius_ctx *c, const crius_cluster *cl,
+                                         const crius_jobs *jb, int32_t job_begin,
+                                         int32_t job_end, void *stream) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  if (job_begin < 0 || job_end > c->P.J || job_begin > job_end)
+    return fail(CRIUS_EINVAL, "update_profiles_range: bad job range");
   if (!cl || !jb || cl->n_types != c->P.T || jb->n_jobs != c->P.J || jb->k_max != c->k_max)
     return fail(CRIUS_EINVAL, "update_profiles: shape differs from the loaded problem");
   crius_config cf{};
@@ -420,10 +439,10 @@ crius_status crius_update_profiles(crius_ctx *c, const crius_cluster *cl, const 
   cudaStream_t st = (cudaStream_t)stream;
   fill_types(c, cl);
   c->Lmax = Lmax;
-  s = copy_inputs(c, cl, jb, st);
+  s = copy_inputs(c, cl, jb, st, job_begin, job_end);
   if (s != CRIUS_OK) return s;
   c->enumerated = false;
-  return finish_load(c, cl, jb, &cf, st);
+  return finish_load(c, cl, jb, &cf, st, job_begin, job_end);
 }
 
 crius_status crius_enumerate_cells(crius_ctx *c, int64_t *n_cells, int64_t *n_plans,

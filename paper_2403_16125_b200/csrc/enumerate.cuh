@@ -203,8 +203,8 @@ __global__ void k_priority_scatter(const int32_t *rank, int32_t J, int32_t *pi) 
 
 // Device-side profile validation: min over c (must be >= 1) and per-job max c
 // (for the §N0 bound L*max(c)*GB < 2^52, checked on the host).
-__global__ void k_profile_stats(Params P, int32_t *job_maxc, int32_t *min_c) {
-  const int j = blockIdx.x;
+__global__ void k_profile_stats(Params P, int j0, int32_t *job_maxc, int32_t *min_c) {
+  const int j = j0 + blockIdx.x;
   const int64_t off = P.off[j];
   const int L = P.L[j];
   int mx = 0, mn = INT32_MAX;

@@ -24,6 +24,14 @@ class ShardPlan:
         self.chunk = int(max(self.cell_begin[r + 1] - self.cell_begin[r] for r in range(world)))
         self.n_cells = int(self.cell_begin[world])
 
+    def job_range(self, rank, n_types):
+        """Jobs whose units (job * n_types + type) fall in rank's unit range: the
+        per-layer profile rows that rank needs (crius_update_profiles_range)."""
+        u0, u1 = int(self.unit_begin[rank]), int(self.unit_begin[rank + 1])
+        if u1 <= u0:
+            return 0, 0
+        return u0 // n_types, (u1 + n_types - 1) // n_types
+
 
 def estimate_all(ctx, plan: ShardPlan, rank, mine=None, gathered=None, full=None, group=None):
     """Estimate this rank's range, all-gather all ranks' records, compact.

@@ -247,6 +247,32 @@ def test_update_profiles_and_repeat(crius, oracle_mod):
     assert np.array_equal(r2, t_ns)
 
 
+def test_update_profiles_range(crius, oracle_mod):
+    """crius_update_profiles_range: only the rows of jobs [j0, j1) change; the
+    Cells of those jobs must match the oracle on the new values, the others the
+    oracle on the old ones (their rows were not re-copied)."""
+    pkg = crius
+    a, b = W.make_config(3, seed=3), W.make_config(3, seed=3)
+    b.c = (b.c * 2).astype(np.int32)
+    b.bnd = b.bnd + 7
+    j0, j1 = 300, 650
+    with pkg.Crius(a) as cr:
+        cr.enumerate()
+        cr.update(b, j0, j1)
+        n, _, _ = cr.enumerate()
+        cells = {k: v.cpu().numpy() for k, v in cr.cells().items()}
+        got = pkg.decode(cr.estimate())[0][:n]
+    _, _, t_a, _, _ = oracle_run(oracle_mod, a)
+    _, _, t_b, _, _ = oracle_run(oracle_mod, b)
+    inr = (cells["job"] >= j0) & (cells["job"] < j1)
+    assert inr.any() and (~inr).any()
+    assert np.array_equal(got[inr], t_b[inr])
+    assert np.array_equal(got[~inr], t_a[~inr])
+    with pkg.Crius(a) as cr:
+        with pytest.raises(pkg.CriusError):
+            cr.update(b, 5, a.n_jobs + 1)
+
+
 def test_loader_rejects_overflow(crius):
     pkg = crius
     pr = W.make_config(2)
