@@ -184,52 +184,6 @@ crius_status validate_static(const crius_cluster *cl, const crius_jobs *jb, cons
   return CRIUS_OK;
 }
 
-// §N0 bounds with the per-job max of c measured on the device.
-crius_status validate_bounds(const crius_cluster *cl, const crius_jobs *jb, const crius_config *cf,
-                             const std::vector<int32_t> &maxc, int32_t minc, int j0, int j1) {
-  typedef __int128 i128;
-  if (minc < 1) return fail(CRIUS_EINVAL, "compute_ns must be >= 1 everywhere");
-  const i128 LIM52 = (i128)1 << 52, LIM62 = (i128)1 << 62, LIM63 = (i128)1 << 63, MIB = 1 << 20;
-  i128 amax = 0, bmax = 0;
-  for (int t = 0; t < cl->n_types; ++t) {
-    amax = std::max<i128>(amax, std::max(cl->alpha_intra_ns[t], cl->alpha_inter_ns[t]));
-    bmax = std::max<i128>(bmax, std::max(cl->beta_intra_ns_per_mib[t], cl->beta_inter_ns_per_mib[t]));
-  }
-  const i128 p = cf->g_max;  // tp, dp <= g <= g_max
-  for (int j = j0; j < j1; ++j) {
-    auto js = [j] { return "job " + std::to_string(j); };
-    const int64_t o = jb->layer_off[j];
-    const i128 L = jb->n_layers[j], GB = jb->global_batch[j];
-    i128 W = 0, A = 0, V = 0, N = 0, Bm = 0;
-    for (int l = 0; l < L; ++l) {
-      const int64_t w = jb->param_bytes[o + l], a = jb->act_bytes[o + l];
-      const int64_t bd = jb->boundary_bytes[o + l], tv = jb->tp_bytes[o + l];
-      const int32_t tn = jb->tp_calls[o + l];
-      if (w < 0 || a < 0 || bd < 0 || tv < 0 || tn < 0)
-        return fail(CRIUS_EINVAL, js() + ": negative per-layer value");
-      W += w;
-      A += a;
-      V += tv;
-      N += tn;
-      Bm = std::max<i128>(Bm, bd);
-    }
-    if (L * maxc[j] * GB >= LIM52) return fail(CRIUS_EINVAL, js() + ": L*max(c)*GB >= 2^52");
-    if (2 * (p - 1) * GB * V >= LIM63 || p * GB * Bm >= LIM63 || 2 * (p - 1) * W >= LIM63)
-      return fail(CRIUS_EINVAL, js() + ": alpha-beta numerator >= 2^63");
-    if ((i128)jb->k_state[j] * W + GB * A >= LIM62)
-      return fail(CRIUS_EINVAL, js() + ": kst*sum(w) + GB*sum(act) >= 2^62");
-    const i128 comp = GB * L * maxc[j];
-    const i128 tpc = N * 2 * (p - 1) * amax + L * (2 * (p - 1) * GB * V * bmax / MIB + 1);
-    const i128 inb = L * (amax + GB * Bm * bmax / MIB + 1 + (p - 1) * amax + (p - 1) * GB * Bm * bmax / MIB + 1);
-    const i128 X = comp + tpc + inb;
-    const i128 sync = 2 * (p - 1) * amax + 2 * (p - 1) * W * bmax / MIB + 1;
-    i128 Bmax = 4 * std::min<i128>(L, cf->s_max);
-    if (cf->b_mode == 1) Bmax = cf->b_values[cf->b_count - 1];
-    if (Bmax * X + sync >= LIM62) return fail(CRIUS_EINVAL, js() + ": T_iter bound >= 2^62");
-  }
-  return CRIUS_OK;
-}
-
 crius_status copy_inputs(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
                          cudaStream_t st, int j0, int j1) {
   const int J = jb->n_jobs, T = cl->n_types;
@@ -282,7 +236,15 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
   int32_t big = INT32_MAX;
   CK(cudaMemcpyAsync(c->d_scratch + J, &big, 4, cudaMemcpyHostToDevice, st));
   if (j1 > j0) {
-    k_profile_stats<<<j1 - j0, 64, 0, st>>>(c->P, j0, c->d_scratch, c->d_scratch + J);
+    BoundArgs BA{};
+    for (int t = 0; t < cl->n_types; ++t) {
+      BA.amax = std::max<int64_t>(BA.amax, std::max(cl->alpha_intra_ns[t], cl->alpha_inter_ns[t]));
+      BA.bmax = std::max<int64_t>(BA.bmax, std::max(cl->beta_intra_ns_per_mib[t],
+                                                    cl->beta_inter_ns_per_mib[t]));
+    }
+    BA.p = cf->g_max;
+    BA.bmax_list = cf->b_mode == 1 ? cf->b_values[cf->b_count - 1] : 0;
+    k_profile_check<<<j1 - j0, 64, 0, st>>>(c->P, j0, BA, c->d_scratch, c->d_scratch + J);
     CKL();
   }
   CK(cudaMemsetAsync(c->d_rank, 0, (size_t)J * 4, st));
@@ -291,12 +253,18 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
   CKL();
   k_priority_scatter<<<tiles, 256, 0, st>>>(c->d_rank, J, c->d_pi);
   CKL();
-  c->launches += 3;
+  c->launches += 2 + (j1 > j0);
   std::vector<int32_t> stats(J + 1);
   CK(cudaMemcpyAsync(stats.data(), c->d_scratch, (J + 1) * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  std::vector<int32_t> maxc(stats.begin(), stats.begin() + J);
-  return validate_bounds(cl, jb, cf, maxc, j1 > j0 ? stats[J] : 1, j0, j1);
+  if (j1 > j0 && stats[J] < 1) return fail(CRIUS_EINVAL, "compute_ns must be >= 1 everywhere");
+  static const char *why[] = {"", "negative per-layer value", "L*max(c)*GB >= 2^52",
+                              "alpha-beta numerator >= 2^63", "kst*sum(w) + GB*sum(act) >= 2^62",
+                              "T_iter bound >= 2^62"};
+  for (int j = j0; j < j1; ++j)
+    if (stats[j] != 0)
+      return fail(CRIUS_EINVAL, "job " + std::to_string(j) + ": " + why[std::min(stats[j], 5)]);
+  return CRIUS_OK;
 }
 
 }  // namespace

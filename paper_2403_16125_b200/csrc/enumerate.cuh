@@ -201,13 +201,38 @@ __global__ void k_priority_scatter(const int32_t *rank, int32_t J, int32_t *pi) 
   if (j < J) pi[rank[j]] = j;
 }
 
-// Device-side profile validation: min over c (must be >= 1) and per-job max c
-// (for the §N0 bound L*max(c)*GB < 2^52, checked on the host).
-__global__ void k_profile_stats(Params P, int j0, int32_t *job_maxc, int32_t *min_c) {
+// Device-side profile validation, one block per job of [j0, j0 +
+// gridDim.x): the job's max over c (every type and plane), min over c, and the
+// per-layer sums; thread 0 then evaluates the overflow bounds of the plan
+// cost and writes code[j]: 0 ok, 1 negative per-layer value, 2 L*max(c)*GB >=
+// 2^52, 3 an alpha-beta numerator >= 2^63, 4 kst*sum(w) + GB*sum(act) >=
+// 2^62, 5 the T_iter bound >= 2^62.  min_c collects the global min of c.
+struct BoundArgs {
+  int64_t amax, bmax;  // max alpha / beta over types and link classes
+  int64_t p;           // g_max (tp, dp <= g <= g_max)
+  int64_t bmax_list;   // b_mode 1: largest B; 0: B = 4 min(L, s_max)
+};
+
+__device__ __forceinline__ __int128 warp_sum128(__int128 x) {
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)x, d);
+    const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(x >> 64), d);
+    x += ((__int128)hi << 64) | (__int128)lo;
+  }
+  return x;
+}
+
+// blockDim.x == 64 (two warps)
+__global__ void __launch_bounds__(64) k_profile_check(Params P, int j0, BoundArgs BA, int32_t *code,
+                                                      int32_t *min_c) {
+  typedef __int128 i128;
+  __shared__ i128 s_sum[2][4];
+  __shared__ int s_mx[2], s_mn[2], s_neg[2];
+  __shared__ long long s_bm[2];
   const int j = j0 + blockIdx.x;
   const int64_t off = P.off[j];
   const int L = P.L[j];
-  int mx = 0, mn = INT32_MAX;
+  int mx = 0, mn = INT32_MAX, neg = 0;
   for (int tk = 0; tk < P.T * P.K1; ++tk) {
     const int32_t *row = P.c + (int64_t)tk * P.TL + off;
     for (int l = threadIdx.x; l < L; l += blockDim.x) {
@@ -215,13 +240,70 @@ __global__ void k_profile_stats(Params P, int j0, int32_t *job_maxc, int32_t *mi
       mn = min(mn, row[l]);
     }
   }
+  i128 W = 0, A = 0, V = 0, N = 0;  // exact: at most 4 values per thread, then 128-bit sums
+  long long Bm = 0;
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    const int64_t w = P.w[off + l], a = P.act[off + l], bd = P.bnd[off + l], tv = P.tpv[off + l];
+    const int32_t tn = P.tpn[off + l];
+    neg |= (w < 0) | (a < 0) | (bd < 0) | (tv < 0) | (tn < 0);
+    W += w;
+    A += a;
+    V += tv;
+    N += tn;
+    Bm = max(Bm, (long long)bd);
+  }
   for (int d = 16; d > 0; d >>= 1) {
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+    neg |= __shfl_xor_sync(0xffffffffu, neg, d);
+    Bm = max(Bm, __shfl_xor_sync(0xffffffffu, Bm, d));
   }
-  if ((threadIdx.x & 31) == 0) {
-    atomicMax(&job_maxc[j], mx);
+  W = warp_sum128(W);
+  A = warp_sum128(A);
+  V = warp_sum128(V);
+  N = warp_sum128(N);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_mx[wid] = mx;
+    s_mn[wid] = mn;
+    s_neg[wid] = neg;
+    s_bm[wid] = Bm;
+    s_sum[wid][0] = W;
+    s_sum[wid][1] = A;
+    s_sum[wid][2] = V;
+    s_sum[wid][3] = N;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mx = max(s_mx[0], s_mx[1]);
+    mn = min(s_mn[0], s_mn[1]);
+    neg = s_neg[0] | s_neg[1];
+    Bm = max(s_bm[0], s_bm[1]);
+    const i128 Ws = s_sum[0][0] + s_sum[1][0], As = s_sum[0][1] + s_sum[1][1];
+    const i128 Vs = s_sum[0][2] + s_sum[1][2], Ns = s_sum[0][3] + s_sum[1][3];
     atomicMin(min_c, mn);
+    const i128 LIM52 = (i128)1 << 52, LIM62 = (i128)1 << 62, LIM63 = (i128)1 << 63, MIB = 1 << 20;
+    const i128 GB = P.gb[j], Li = L, p = BA.p, amax = BA.amax, bmax = BA.bmax;
+    int c = 0;
+    if (neg) {
+      c = 1;
+    } else if (Li * mx * GB >= LIM52) {
+      c = 2;
+    } else if (2 * (p - 1) * GB * Vs >= LIM63 || p * GB * Bm >= LIM63 || 2 * (p - 1) * Ws >= LIM63) {
+      c = 3;
+    } else if ((i128)P.kst[j] * Ws + GB * As >= LIM62) {
+      c = 4;
+    } else {
+      const i128 comp = GB * Li * mx;
+      const i128 tpc = Ns * 2 * (p - 1) * amax + Li * (2 * (p - 1) * GB * Vs * bmax / MIB + 1);
+      const i128 inb = Li * (amax + GB * Bm * bmax / MIB + 1 + (p - 1) * amax +
+                             (p - 1) * GB * Bm * bmax / MIB + 1);
+      const i128 X = comp + tpc + inb;
+      const i128 sync = 2 * (p - 1) * amax + 2 * (p - 1) * Ws * bmax / MIB + 1;
+      const i128 Bmax = BA.bmax_list ? (i128)BA.bmax_list : (i128)4 * min(L, P.s_max);
+      if (Bmax * X + sync >= LIM62) c = 5;
+    }
+    code[j] = c;
   }
 }
 

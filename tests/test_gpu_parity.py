@@ -283,6 +283,33 @@ def test_loader_rejects_overflow(crius):
     assert e.value.code == 2 and "2^52" in str(e.value)
 
 
+@pytest.mark.parametrize("field,value,msg", [("c", 0, "compute_ns must be >= 1"),
+                                             ("w", -1, "negative per-layer value"),
+                                             ("act", 2 ** 58, "kst*sum(w) + GB*sum(act) >= 2^62"),
+                                             ("tpv", 2 ** 58, "alpha-beta numerator >= 2^63")])
+def test_loader_rejects_per_layer(crius, field, value, msg):
+    """The §N0 checks run on the device per job (k_profile_check); a violation
+    names the job and the bound, and the range update checks only its rows."""
+    pkg = crius
+    pr = W.make_config(2)
+    bad = getattr(pr, field).copy()
+    if field == "c":
+        bad[0, 0, pr.layer_off[3]] = value
+    else:
+        bad[pr.layer_off[3]] = value
+    setattr(pr, field, bad)
+    with pytest.raises(pkg.CriusError) as e:
+        pkg.Crius(pr)
+    assert e.value.code == 2 and msg in str(e.value)
+    if field != "c":
+        assert "job 3" in str(e.value)
+    good = W.make_config(2)
+    with pkg.Crius(good) as cr:
+        cr.update(pr, 4, pr.n_jobs)       # rows of job 3 are not re-checked
+        with pytest.raises(pkg.CriusError):
+            cr.update(pr, 0, pr.n_jobs)
+
+
 def test_cfg5_x10_sampled_units(crius, oracle_mod):
     """100k-job stress (414 M plans): the GPU estimates everything; the oracle
     re-derives the Cell table and recomputes 60 sampled units one by one."""
