@@ -210,21 +210,40 @@ __device__ __forceinline__ int64_t plan_group_time(const UnitCtx &U, int G, int 
         Zh = __umul64hi(z, b_tp);
       }
     }
+    // The B values of a group ascend, so mb = 2^lm descends and every term's
+    // exponent e = k + 20 - lm grows from one B to the next: after the first
+    // 128-bit ceil-shift the next is ceil(r / 2^(e - e_prev)) of the 64-bit
+    // result (ceil(ceil(x / 2^a) / 2^b) = ceil(x / 2^(a+b)) for x >= 0).
+    uint64_t rX = 0, rY = 0, rZ = 0;
+    int pe = 0;
+    bool chain = false, chainY = false;
 #pragma unroll
     for (int q = 0; q < NBG; ++q) {
       if (!ok[q]) continue;
       const int lm = lmb[q];
+      const int e = k + 20 - lm;
+      const int d = e - pe;
       uint64_t T = (uint64_t)C << lm;
-      if (k) T += tpn_alpha + ceil_shr128(Xh, Xl, k + 20 - lm);
+      if (k) {
+        rX = chain ? (rX + (1ull << d) - 1) >> d : ceil_shr128(Xh, Xl, e);
+        T += tpn_alpha + rX;
+      }
       if (s) {
-        if (lm >= k) {
-          T += a_b + ceil_shr128(Yh, Yl, 20 - (lm - k));
+        if (lm >= k) {  // exponent 20 - (lm - k) == e
+          rY = chainY ? (rY + (1ull << d) - 1) >> d : ceil_shr128(Yh, Yl, e);
+          chainY = true;
+          T += a_b + rY;
         } else {
           const int sh = k - lm;
           T += a_b + mul_shr_ceil((bnd + (1ull << sh) - 1) >> sh, b_b, 20);
         }
-        if (k) T += (tp - 1) * a_tp + ceil_shr128(Zh, Zl, k + 20 - lm);
+        if (k) {
+          rZ = chain ? (rZ + (1ull << d) - 1) >> d : ceil_shr128(Zh, Zl, e);
+          T += (tp - 1) * a_tp + rZ;
+        }
       }
+      chain = true;
+      pe = e;
       sumT[q] += (int64_t)T;
       maxT[q] = max(maxT[q], (int64_t)T);
     }
