@@ -648,7 +648,8 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   else if (amode == 3)
     kern = warps == 4 ? k_estimate<4, 1, 3> : k_estimate<1, 1, 3>;
   else
-    kern = warps == 4 ? k_estimate<4, 1, 4> : k_estimate<1, 1, 4>;
+    kern = warps == 4 ? (wide ? k_estimate<4, CRIUS_NBG_WIDE, 4> : k_estimate<4, 1, 4>)
+                      : (wide ? k_estimate<1, CRIUS_NBG_WIDE, 4> : k_estimate<1, 1, 4>);
   int per_sm = 1;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));

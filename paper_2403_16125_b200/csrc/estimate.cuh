@@ -532,51 +532,125 @@ __device__ void paper_gpus_lane(const int64_t *P, const int16_t *bd, int S, int 
   }
 }
 
-// T_iter of plan (k, lB) over stages with GPU counts g (R-10): uniform tp = 2^k,
-// dp_s = g_s / tp, mb_s = GB/(B dp_s); GPUs packed from a node boundary in
-// stage order (offset o): tp intra iff tp <= gpn and tp | o; dp intra iff the
-// stage lies in one node; boundary into s intra iff o is not a node boundary.
-__device__ __forceinline__ int64_t paper_plan_time(const UnitCtx &U, const int16_t *bd,
-                                                   const int32_t *g, int S, int k, int lB,
-                                                   int gpn) {
+// NEXT-2 plan cost (R-10): uniform tp = 2^k (k <= log2 min g_s), dp_s = g_s / tp,
+// mb_s = GB/(B dp_s); GPUs packed from a node boundary in stage order (offset
+// o): tp intra iff tp <= gpn and tp | o; dp intra iff the stage lies in one
+// node; boundary into s intra iff o is not a node boundary.
+// NBG microbatch counts at once (the B-independent per-stage work --
+// links, memory, sync, the 128-bit alpha-beta products -- done once per stage;
+// per B the ceil-shifts are chained as in plan_group_time).  Returns the best
+// (T, p) of plan group (k, bg), lowest p on ties.
+template <int NBG>
+__device__ __forceinline__ int64_t paper_plan_group_time(const UnitCtx &U, const int16_t *bd,
+                                                         const int32_t *g, int S, int k, int bg,
+                                                         int gpn, int &best_p) {
+  const int lS = ilog2_pow2(S);
+  int lB[NBG];
+  bool ok[NBG];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < NBG; ++q) {
+    const int b = bg * NBG + q;
+    lB[q] = U.b_mode == 0 ? lS + 2 : (b < U.nB ? U.lBv[b] : 0);
+    ok[q] = U.b_mode == 0 ? q == 0 : b < U.nB;
+    any |= ok[q];
+  }
+  if (!any) return kInf;
   const uint64_t tp = 1ull << k;
-  int64_t sumT = 0, maxT = 0, maxSync = 0;
+  int64_t sumT[NBG], maxT[NBG];
+#pragma unroll
+  for (int q = 0; q < NBG; ++q) sumT[q] = maxT[q] = 0;
+  int64_t maxSync = 0;
   int64_t o = 0;
   const int64_t *PCk = U.PC + k * U.Lp;
   for (int s = 0; s < S; ++s) {
     const int gs = g[s], a = bd[s], e = bd[s + 1];
     const int ldp = ilog2_pow2((uint32_t)gs) - k;
-    if (ldp < 0 || lB + ldp > U.lGB) return kInf;  // tp <= g_s; B dp <= GB (A-12)
-    const int lmb = U.lGB - lB - ldp;
+    if (ldp < 0) return kInf;
     const uint64_t dp = 1ull << ldp;
     const bool tp_in = (int64_t)tp <= gpn && (o & (int64_t)(tp - 1)) == 0;
     const bool dp_in = o / gpn == (o + gs - 1) / gpn;
     const uint64_t a_tp = tp_in ? U.a_in : U.a_x, b_tp = tp_in ? U.b_in : U.b_x;
     const uint64_t a_dp = dp_in ? U.a_in : U.a_x, b_dp = dp_in ? U.b_in : U.b_x;
-    const int64_t W = U.PW[e] - U.PW[a], A = U.PA[e] - U.PA[a];
+    const int64_t W = U.PW[e] - U.PW[a], A = U.PA[e] - U.PA[a], C = PCk[e] - PCk[a];
+    if (ldp > U.lGB) return kInf;  // dp > GB: no microbatch fits any B
     const uint64_t mem = ((uint64_t)(U.kst * W + (A << (U.lGB - ldp))) + tp - 1) >> k;
     if (mem > (uint64_t)U.memt) return kInf;
-    uint64_t T = (uint64_t)(PCk[e] - PCk[a]) << lmb;
-    if (k) {
-      const uint64_t V = (uint64_t)(U.PV[e] - U.PV[a]) << lmb;
-      T += (uint64_t)(U.PN[e] - U.PN[a]) * (2 * (tp - 1)) * a_tp + mul_shr_ceil(2 * (tp - 1) * V, b_tp, k + 20);
-    }
-    if (s) {
-      const uint64_t Vb = (uint64_t)U.BND[a - 1] << lmb;
-      const bool b_in = o % gpn != 0;
-      T += (b_in ? U.a_in : U.a_x) + mul_shr_ceil((Vb + tp - 1) >> k, b_in ? U.b_in : U.b_x, 20);
-      if (k) T += (tp - 1) * a_tp + mul_shr_ceil((tp - 1) * Vb, b_tp, k + 20);
-    }
     if (ldp) {
       const uint64_t Wt = ((uint64_t)W + tp - 1) >> k;
       const uint64_t sy = 2 * (dp - 1) * a_dp + mul_shr_ceil(2 * (dp - 1) * Wt, b_dp, ldp + 20);
       maxSync = max(maxSync, (int64_t)sy);
     }
-    sumT += (int64_t)T;
-    maxT = max(maxT, (int64_t)T);
+    uint64_t Xh = 0, Xl = 0, tpn_alpha = 0;
+    if (k) {
+      const uint64_t x = 2 * (tp - 1) * (uint64_t)(U.PV[e] - U.PV[a]);
+      Xl = x * b_tp;
+      Xh = __umul64hi(x, b_tp);
+      tpn_alpha = (uint64_t)(U.PN[e] - U.PN[a]) * (2 * (tp - 1)) * a_tp;
+    }
+    uint64_t Yh = 0, Yl = 0, Zh = 0, Zl = 0, a_b = 0, b_b = 0, bnd = 0;
+    if (s) {
+      bnd = (uint64_t)U.BND[a - 1];
+      const bool b_in = o % gpn != 0;
+      a_b = b_in ? U.a_in : U.a_x;
+      b_b = b_in ? U.b_in : U.b_x;
+      Yl = bnd * b_b;
+      Yh = __umul64hi(bnd, b_b);
+      if (k) {
+        const uint64_t z = (tp - 1) * bnd;
+        Zl = z * b_tp;
+        Zh = __umul64hi(z, b_tp);
+      }
+    }
+    uint64_t rX = 0, rY = 0, rZ = 0;
+    int pe = 0;
+    bool chain = false, chainY = false;
+#pragma unroll
+    for (int q = 0; q < NBG; ++q) {
+      const int lm = U.lGB - lB[q] - ldp;  // mb_s = GB / (B dp_s)
+      if (lm < 0) ok[q] = false;           // B dp_s > GB (A-12)
+      if (!ok[q]) continue;
+      const int ex = k + 20 - lm;
+      const int d = ex - pe;
+      uint64_t T = (uint64_t)C << lm;
+      if (k) {
+        rX = chain ? (rX + (1ull << d) - 1) >> d : ceil_shr128(Xh, Xl, ex);
+        T += tpn_alpha + rX;
+      }
+      if (s) {
+        if (lm >= k) {
+          rY = chainY ? (rY + (1ull << d) - 1) >> d : ceil_shr128(Yh, Yl, ex);
+          chainY = true;
+          T += a_b + rY;
+        } else {
+          const int sh = k - lm;
+          T += a_b + mul_shr_ceil((bnd + (1ull << sh) - 1) >> sh, b_b, 20);
+        }
+        if (k) {
+          rZ = chain ? (rZ + (1ull << d) - 1) >> d : ceil_shr128(Zh, Zl, ex);
+          T += (tp - 1) * a_tp + rZ;
+        }
+      }
+      chain = true;
+      pe = ex;
+      sumT[q] += (int64_t)T;
+      maxT[q] = max(maxT[q], (int64_t)T);
+    }
     o += gs;
   }
-  return sumT + (int64_t)((1ll << lB) - 1) * maxT + maxSync;
+  int64_t best = kInf;
+  int bq = 0;
+#pragma unroll
+  for (int q = 0; q < NBG; ++q) {
+    if (!ok[q]) continue;
+    const int64_t ti = sumT[q] + (int64_t)((1ll << lB[q]) - 1) * maxT[q] + maxSync;
+    if (ti < best) {
+      best = ti;
+      bq = q;
+    }
+  }
+  best_p = U.b_mode == 0 ? k : k * U.nB + bg * NBG + bq;
+  return best;
 }
 
 // ---- cp.async (LDGSTS) staging: global -> shared without registers ---------
@@ -805,7 +879,16 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
     __syncwarp();
 
     const int nSi = ilog2_pow2(smax) + 1;
-    if (AMODE == 4) {  // NEXT-2: the paper's cuts for every S of the unit
+    // NEXT-2 with every boundary carrying the same bytes (transformer stacks):
+    // every gap ties at beta, none is forced, and the cut rule IS the §N3
+    // min-max split with R0 -- take the D1 path below
+    bool paper_cuts = false;
+    if (AMODE == 4) {
+      bool uneq = false;
+      for (int q = lane; q < L - 1; q += 32) uneq |= BND[q] != BND[0];
+      paper_cuts = __any_sync(0xffffffffu, uneq);
+    }
+    if (paper_cuts) {  // NEXT-2: the paper's cuts for every S of the unit
       // gap bytes sorted ascending (rank by counting; index breaks ties)
       for (int q = lane; q < L - 1; q += 32) {
         const int64_t v = BND[q];
@@ -886,16 +969,17 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
         }
         gmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)gmin);
         gmx = warp_max_int(gmx);
-        const int nitem = gmx > P.g_max ? 0 : (ilog2_pow2((uint32_t)gmin) + 1) * nB;
+        const int ngrp = (nB + NBG - 1) / NBG;
+        const int nitem = gmx > P.g_max ? 0 : (ilog2_pow2((uint32_t)gmin) + 1) * ngrp;
         int64_t bT = kInf;
         int bp = INT32_MAX;
-        for (int it = lane; it < nitem; it += 32) {
-          const int k = it / nB, bi = it - k * nB;
-          const int lB = P.b_mode == 0 ? lS + 2 : P.lB[bi];
-          const int64_t T = paper_plan_time(U, bd, PGS, S, k, lB, gpn);
+        for (int it = lane; it < nitem; it += 32) {  // item = (k, group of NBG B values)
+          const int k = it / ngrp, bgi = it - k * ngrp;
+          int p;
+          const int64_t T = paper_plan_group_time<NBG>(U, bd, PGS, S, k, bgi, gpn, p);
           if (T < bT) {  // items ascending per lane: ties keep the lower p
             bT = T;
-            bp = it;
+            bp = p;
           }
         }
         int64_t wT = bT;
