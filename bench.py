@@ -36,6 +36,17 @@ ALU_OPS_PER_DP_PROBE = 8      # one binary-search probe of the st
 ALU_OPS_PER_STAGE_EVAL = 40   # one (plan, stage) cost evaluation
 SM_COUNT = 148
 INT_LANES_PER_SM = 128
+# k_round_greedy (one CTA, sequential by definition) has no throughput roofline;
+# its floor is its chain of CTA-wide barriers: every Phase A batch needs >= 3,
+# every victim-sequence recomputation >= 4 plus one group barrier per move,
+# every Phase B batch >= 2.  Measured __syncthreads latency at 1024 threads
+# on this B200: 76.9 cycles (profiles/r1_latency_microbench.txt).
+BARRIER_CYCLES = 76.9
+
+
+def round_floor(st, depth, sm_mhz):
+    n = 3 * st["phaseA_batches"] + (4 + depth) * st["seq_recomputes"] + 2 * st["phaseB_batches"]
+    return n, n * BARRIER_CYCLES / (sm_mhz * 1e3)  # barriers, ms
 
 
 def parse():
@@ -458,6 +469,9 @@ def main():
                "h2d_bytes_per_step": int(bytes_t[0]), "d2h_bytes_per_step": int(bytes_t[1]),
                "ms_per_step": e2e_ms}
 
+    rstats = cr.round_stats()
+    n_bar, floor_ms = round_floor(rstats, pr.depth, float(clocks.get("sm_mhz") or 1965.0))
+    round_ms = float(np.median(seg[:, 3]))
     line = {"metric": "Cell-plan evaluations/sec", "value": value, "unit": "cell-plans/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
@@ -475,8 +489,14 @@ def main():
                                         f"sm_max_mhz ({src})",
                          "ops_per_launch": ops * frac_units, "dp_probes": probes,
                          "stage_evals": stage_evals,
-                         "hbm_gbs": hbm, "hbm_frac": hbm / float(peaks.get("hbm_gbs", 6650.0))},
-            "round_stats": cr.round_stats(),
+                         "hbm_gbs": hbm, "hbm_frac": hbm / float(peaks.get("hbm_gbs", 6650.0)),
+                         "dominant": {"kernel": "k_round_greedy", "share": round_ms / ms_per_step,
+                                      "bound": "latency (one CTA: the round is sequential)",
+                                      "barrier_chain": n_bar, "floor_ms": floor_ms,
+                                      "achieved_ms": round_ms, "frac": floor_ms / round_ms,
+                                      "floor_source": f"{n_bar} CTA barriers x {BARRIER_CYCLES} "
+                                                      "cycles (measured) at sm_mhz"}},
+            "round_stats": rstats,
             "clocks": clocks, "gpu_launches": int(launches)}
     if e2e:
         line["e2e"] = e2e
