@@ -457,25 +457,34 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   int32_t *mv = sh.wmv[wid];
   if (lane < TT) f2[lane] = sh.frs[t][0][lane];
   __syncwarp();
+  // each thread's best cached same-type move (i) over its strided jobs only
+  // changes when that job is moved: rescan only then
+  bool hv1 = false;
+  double bk1 = 0.0;
+  int bp1 = 0, bi1 = 0, ba1 = -1;
+  bool rescan = true;
   for (int m = 0; m < R.depth; ++m) {
-    bool have = false;
-    double bk = 0.0;
-    int bp = 0, bi = 0, ba = -1, bidx = -1;
-    for (int a = gt; a < n_adm; a += gn) {  // (i): loads issued together
-      const int ta = A.t[a], bo = A.bi_opt[a], p = A.pos[a];
-      const double k = A.bi_key[a];
-      bool moved = false;
-      for (int q = 0; q < m; ++q) moved |= mv[q] == a;
-      if (ta != t || bo < 0 || moved) continue;
-      if (!have || k < bk || (k == bk && (p < bp || (p == bp && bo < bi)))) {
-        have = true;
-        bk = k;
-        bp = p;
-        bi = bo;
-        ba = a;
-        bidx = -1;
+    if (rescan) {
+      hv1 = false;
+      ba1 = -1;
+      for (int a = gt; a < n_adm; a += gn) {  // (i): loads issued together
+        const int ta = A.t[a], bo = A.bi_opt[a], p = A.pos[a];
+        const double k = A.bi_key[a];
+        bool moved = false;
+        for (int q = 0; q < m; ++q) moved |= mv[q] == a;
+        if (ta != t || bo < 0 || moved) continue;
+        if (!hv1 || k < bk1 || (k == bk1 && (p < bp1 || (p == bp1 && bo < bi1)))) {
+          hv1 = true;
+          bk1 = k;
+          bp1 = p;
+          bi1 = bo;
+          ba1 = a;
+        }
       }
     }
+    bool have = hv1;
+    double bk = bk1;
+    int bp = bp1, bi = bi1, ba = ba1, bidx = -1;
     for (int k = gt; k < nE; k += gn) {  // (ii)
       const int a = list[k];
       const int ta = A.t[a], p = A.pos[a], G2 = E.G2[k], t2 = E.t2[k];
@@ -540,6 +549,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
       if (gwid == 0) sh.frs[t][m + 1][lane] = f;
     }
     if (lane == 0) mv[m] = ca;
+    rescan = ba1 == ca;  // this thread's (i) candidate was moved
     if (gwid == 0 && lane == 0) {  // record move m
       const int idx = sh.g_idx[par][ws];
       const double s2 = idx < 0 ? A.bi_s[ca] : E.s2[idx];
