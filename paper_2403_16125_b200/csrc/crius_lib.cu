@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/crius.h"
 #include "common.cuh"
 #include "enumerate.cuh"
@@ -69,6 +71,10 @@ struct crius_ctx {
   int32_t *d_c = nullptr, *d_tpn = nullptr;
   int64_t *d_w = nullptr, *d_act = nullptr, *d_bnd = nullptr, *d_tpv = nullptr;
   int32_t *d_rank = nullptr, *d_pi = nullptr;
+  int64_t *d_pkeys = nullptr;     // [2J] priority sort keys (double buffer)
+  int32_t *d_pvals = nullptr;     // [2J] priority sort values
+  void *d_sort_tmp = nullptr;     // cub radix-sort scratch
+  size_t sort_tmp_bytes = 0;
   int32_t *d_scratch = nullptr;  // [J + 8] stats
   // host copies needed later
   std::vector<int32_t> cap;
@@ -103,6 +109,7 @@ namespace {
 void free_all(crius_ctx *c) {
   void *ptrs[] = {c->d_ng, c->d_gb, c->d_kst, c->d_L, c->d_off, c->d_submit, c->d_id, c->d_c,
                   c->d_tpn, c->d_w, c->d_act, c->d_bnd, c->d_tpv, c->d_rank, c->d_pi,
+                  c->d_pkeys, c->d_pvals, c->d_sort_tmp,
                   c->d_scratch, c->C.job, c->C.type, c->C.G, c->C.S, c->C.nplans, c->C.plan_off,
                   c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight,
                   c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
@@ -247,13 +254,43 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
     k_profile_check<<<j1 - j0, 64, 0, st>>>(c->P, j0, BA, c->d_scratch, c->d_scratch + J);
     CKL();
   }
-  CK(cudaMemsetAsync(c->d_rank, 0, (size_t)J * 4, st));
+  // priority order: stable radix sort by id, then by submit (A-18); only the
+  // key bits in use are sorted (non-negative keys: the sign bit never differs)
+  auto key_bits = [J](const int64_t *k) {
+    int64_t mn = 0, mx = 0;
+    for (int j = 0; j < J; ++j) {
+      mn = std::min(mn, k[j]);
+      mx = std::max(mx, k[j]);
+    }
+    if (mn < 0) return 64;
+    int b = 1;
+    while (b < 63 && (mx >> b) != 0) ++b;
+    return b;
+  };
+  const int bits_id = key_bits(jb->job_id), bits_sub = key_bits(jb->submit_time);
   const unsigned tiles = (unsigned)((J + 255) / 256);
-  k_priority_count<<<dim3(tiles, tiles), 256, 0, st>>>(c->d_submit, c->d_id, J, c->d_rank);
+  int64_t *ka = c->d_pkeys, *kb = c->d_pkeys + J;
+  int32_t *va = c->d_pvals, *vb = c->d_pvals + J;
+  for (int bits : {bits_id, bits_sub}) {  // scratch for these bit ranges (normally <= the load-time query)
+    size_t need = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, ka, kb, va, vb, J, 0, bits, st));
+    if (need > c->sort_tmp_bytes) {
+      CK(cudaFree(c->d_sort_tmp));
+      CK(cudaMalloc(&c->d_sort_tmp, need));
+      c->sort_tmp_bytes = need;
+    }
+  }
+  k_priority_keys_id<<<tiles, 256, 0, st>>>(c->d_id, J, ka, va);
   CKL();
-  k_priority_scatter<<<tiles, 256, 0, st>>>(c->d_rank, J, c->d_pi);
+  size_t tb = c->sort_tmp_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, tb, ka, kb, va, vb, J, 0, bits_id, st));
+  k_priority_keys_submit<<<tiles, 256, 0, st>>>(c->d_submit, vb, J, ka);
   CKL();
-  c->launches += 2 + (j1 > j0);
+  tb = c->sort_tmp_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, tb, ka, kb, vb, va, J, 0, bits_sub, st));
+  k_priority_scatter<<<tiles, 256, 0, st>>>(va, J, c->d_pi, c->d_rank);
+  CKL();
+  c->launches += 5 + (j1 > j0);
   std::vector<int32_t> stats(J + 1);
   CK(cudaMemcpyAsync(stats.data(), c->d_scratch, (J + 1) * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -349,6 +386,12 @@ crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cl, const
   CKA(dalloc(&c->d_tpn, TL));
   CKA(dalloc(&c->d_rank, J));
   CKA(dalloc(&c->d_pi, J));
+  CKA(dalloc(&c->d_pkeys, 2 * (size_t)J));
+  CKA(dalloc(&c->d_pvals, 2 * (size_t)J));
+  CKA(cub::DeviceRadixSort::SortPairs(nullptr, c->sort_tmp_bytes, (int64_t *)nullptr,
+                                      (int64_t *)nullptr, (int32_t *)nullptr, (int32_t *)nullptr,
+                                      J, 0, 64));
+  CKA(cudaMalloc(&c->d_sort_tmp, std::max<size_t>(c->sort_tmp_bytes, 16)));
   CKA(dalloc(&c->d_scratch, J + 8));
   CKA(dalloc(&c->d_counter, 4));
   CKA(dalloc(&c->d_part, 2 * 9 + 2));

@@ -176,29 +176,31 @@ __global__ void k_unit_fill(Params P, Cells C, int64_t n_units) {
   }
 }
 
-// Round priority pi (A-18): rank[j] = #{i : (submit_i, id_i) < (submit_j, id_j)};
-// pi[rank[j]] = j (ids are unique -> a permutation).  2-D tiled all-pairs count:
-// block (x, y) compares the 256 jobs of tile x with the 256 jobs of tile y.
-__global__ void __launch_bounds__(256) k_priority_count(const int64_t *submit, const int64_t *id,
-                                                        int32_t J, int32_t *rank) {
-  __shared__ int64_t ss[256], si[256];
-  const int j = blockIdx.x * 256 + threadIdx.x;
-  const int i0 = blockIdx.y * 256;
-  const int i = i0 + threadIdx.x;
-  ss[threadIdx.x] = i < J ? submit[i] : INT64_MAX;
-  si[threadIdx.x] = i < J ? id[i] : INT64_MAX;
-  __syncthreads();
-  if (j >= J) return;
-  const int64_t mys = submit[j], myi = id[j];
-  const int n = min(256, J - i0);
-  int r = 0;
-  for (int q = 0; q < n; ++q) r += (ss[q] < mys) || (ss[q] == mys && si[q] < myi);
-  if (r) atomicAdd(&rank[j], r);
+// Round priority pi (A-18): jobs ordered by (submit, id) ascending (ids are
+// unique, so the order is total).  Two stable radix sorts (cub): by id, then
+// by submit; these kernels stage the keys and scatter the result:
+// pi[pos] = j and rank[j] = pos.
+__global__ void k_priority_keys_id(const int64_t *id, int32_t J, int64_t *keys, int32_t *vals) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < J) {
+    keys[j] = id[j];
+    vals[j] = j;
+  }
 }
 
-__global__ void k_priority_scatter(const int32_t *rank, int32_t J, int32_t *pi) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < J) pi[rank[j]] = j;
+__global__ void k_priority_keys_submit(const int64_t *submit, const int32_t *by_id, int32_t J,
+                                       int64_t *keys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < J) keys[i] = submit[by_id[i]];
+}
+
+__global__ void k_priority_scatter(const int32_t *order, int32_t J, int32_t *pi, int32_t *rank) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos < J) {
+    const int j = order[pos];
+    pi[pos] = j;
+    rank[j] = pos;
+  }
 }
 
 // Device-side profile validation, one block per job of [j0, j0 +
