@@ -502,9 +502,12 @@ __device__ void paper_gpus_lane(const int64_t *P, const int16_t *bd, int S, int 
   for (int s = 0; s < S; ++s) {
     const __int128 num = (__int128)G * (P[bd[s + 1]] - P[bd[s]]);
     int v = 1;
-    if (num >= F) {
-      int a = 0;
-      while (((__int128)2 << a) * F <= num) ++a;
+    if (num >= F) {  // a = floor(log2(num / F)) from the bit lengths, one correction
+      const uint64_t nhi = (uint64_t)(num >> 64), nlo = (uint64_t)num;
+      const int lnum = nhi ? 127 - __clzll((long long)nhi) : 63 - __clzll((long long)nlo);
+      const int lF = 63 - __clzll((long long)(uint64_t)F);
+      int a = lnum - lF;
+      if ((F << a) > num) --a;
       v = (2 * num >= 3 * ((__int128)1 << a) * F) ? (2 << a) : (1 << a);
     }
     g[s] = v;
@@ -530,6 +533,73 @@ __device__ void paper_gpus_lane(const int64_t *P, const int16_t *bd, int S, int 
     sum += g[w];
     g[w] *= 2;
   }
+}
+
+// The same with lanes = stages (S <= 32): the rounding in parallel, each
+// repair step's argmin / argmax of F_s/g_s (exact 128-bit cross products,
+// ties to the earliest stage) by a shuffle tournament.
+__device__ __forceinline__ int paper_pick(bool elig, int64_t F, int g, bool want_max) {
+  const int lane = threadIdx.x & 31;
+  int s = lane;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const int64_t oF = __shfl_xor_sync(0xffffffffu, F, d);
+    const int og = __shfl_xor_sync(0xffffffffu, g, d);
+    const int os = __shfl_xor_sync(0xffffffffu, s, d);
+    const bool oe = __shfl_xor_sync(0xffffffffu, elig, d);
+    bool take = false;
+    if (oe) {
+      if (!elig) {
+        take = true;
+      } else {
+        const __int128 mine = (__int128)F * og, other = (__int128)oF * g;  // F/g vs oF/og
+        take = want_max ? (other > mine || (other == mine && os < s))
+                        : (other < mine || (other == mine && os < s));
+      }
+    }
+    if (take) {
+      F = oF;
+      g = og;
+      s = os;
+      elig = oe;
+    }
+  }
+  return elig ? s : -1;
+}
+
+__device__ void paper_gpus_warp(const int64_t *P, const int16_t *bd, int S, int G, int32_t *gout,
+                                int lane) {
+  const __int128 Ft = P[bd[S]] - P[bd[0]];
+  int64_t F = 0;
+  int g = 0;
+  if (lane < S) {
+    F = P[bd[lane + 1]] - P[bd[lane]];
+    const __int128 num = (__int128)G * F;
+    g = 1;
+    if (num >= Ft) {
+      const uint64_t nhi = (uint64_t)(num >> 64), nlo = (uint64_t)num;
+      const int lnum = nhi ? 127 - __clzll((long long)nhi) : 63 - __clzll((long long)nlo);
+      const int lF = 63 - __clzll((long long)(uint64_t)Ft);
+      int a = lnum - lF;
+      if ((Ft << a) > num) --a;
+      g = (2 * num >= 3 * ((__int128)1 << a) * Ft) ? (2 << a) : (1 << a);
+    }
+  }
+  int sum = __reduce_add_sync(0xffffffffu, (unsigned)g);
+  while (sum > G) {
+    const int w = paper_pick(lane < S && g >= 2, F, g, false);
+    const int gw = __shfl_sync(0xffffffffu, g, w);
+    if (lane == w) g /= 2;
+    sum -= gw / 2;
+  }
+  while (sum < G) {
+    const int w = paper_pick(lane < S && sum + g <= G, F, g, true);
+    const int gw = __shfl_sync(0xffffffffu, g, w);
+    if (lane == w) g *= 2;
+    sum += gw;
+  }
+  if (lane < S) gout[lane] = g;
+  __syncwarp();
 }
 
 // NEXT-2 plan cost (R-10): uniform tp = 2^k (k <= log2 min g_s), dp_s = g_s / tp,
@@ -569,7 +639,7 @@ __device__ __forceinline__ int64_t paper_plan_group_time(const UnitCtx &U, const
     if (ldp < 0) return kInf;
     const uint64_t dp = 1ull << ldp;
     const bool tp_in = (int64_t)tp <= gpn && (o & (int64_t)(tp - 1)) == 0;
-    const bool dp_in = o / gpn == (o + gs - 1) / gpn;
+    const bool dp_in = (o >> U.lgpn) == ((o + gs - 1) >> U.lgpn);  // gpn = 2^lgpn
     const uint64_t a_tp = tp_in ? U.a_in : U.a_x, b_tp = tp_in ? U.b_in : U.b_x;
     const uint64_t a_dp = dp_in ? U.a_in : U.a_x, b_dp = dp_in ? U.b_in : U.b_x;
     const int64_t W = U.PW[e] - U.PW[a], A = U.PA[e] - U.PA[a], C = PCk[e] - PCk[a];
@@ -591,7 +661,7 @@ __device__ __forceinline__ int64_t paper_plan_group_time(const UnitCtx &U, const
     uint64_t Yh = 0, Yl = 0, Zh = 0, Zl = 0, a_b = 0, b_b = 0, bnd = 0;
     if (s) {
       bnd = (uint64_t)U.BND[a - 1];
-      const bool b_in = o % gpn != 0;
+      const bool b_in = (o & (gpn - 1)) != 0;
       a_b = b_in ? U.a_in : U.a_x;
       b_b = b_in ? U.b_in : U.b_x;
       Yl = bnd * b_b;
@@ -960,8 +1030,12 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
       for (int ci = 0; ci < nc; ++ci) {
         const int G = CG[ci], S = CS[ci], lS = ilog2_pow2(S);
         const int16_t *bd = BD + (S - 1) + lS;
-        if (lane == 0) paper_gpus_lane(PC, bd, S, G, PGS);
-        __syncwarp();
+        if (S <= 32) {
+          paper_gpus_warp(PC, bd, S, G, PGS, lane);
+        } else {
+          if (lane == 0) paper_gpus_lane(PC, bd, S, G, PGS);
+          __syncwarp();
+        }
         int gmin = INT32_MAX, gmx = 0;
         for (int s = lane; s < S; s += 32) {
           gmin = min(gmin, PGS[s]);
