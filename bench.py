@@ -231,7 +231,7 @@ def run_reference(a, rank, world):
             "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded)",
             "config": config_dict(a, pr, n, p, world, False),
             "cpu_baseline": {"value": value, "unit": "cell-plans/s", "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": host_cpu()},
             "e2e": {"value": value, "unit": "cell-plans/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -268,9 +268,28 @@ def cpu_parallel(pr, cells, c1):
             "sample": f"estimate of Cells [0, {c1}) on {len(ranges)} processes, no round"}
 
 
+def host_cpu():
+    """The host CPU model name (report it beside the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(a, pr):
     """The oracle as it stands on this host, one core, bounded sample (~10-30 s);
     plus its estimation sharded over every host core."""
+    out = _cpu_baseline(a, pr)
+    out["cpu_model"] = host_cpu()
+    out["host_threads"] = os.cpu_count()
+    return out
+
+
+def _cpu_baseline(a, pr):
     import oracle
     oracle.build()
     o = oracle.Oracle(pr)
@@ -480,6 +499,9 @@ def main():
             "breakdown_ms": {"enumerate": float(np.median(seg[:, 0])), "estimate": est_ms,
                              "gather": float(np.median(seg[:, 2])),
                              "round": float(np.median(seg[:, 3]))},
+            "latency_ms": {"p10": float(np.percentile(step_ms, 10)),
+                           "p50": float(np.median(step_ms)),
+                           "p90": float(np.percentile(step_ms, 90))},
             "estimate_evals_per_s": n_plans * frac_units / (est_ms / 1e3),
             "roofline": {"kernel": "k_estimate", "bound": "alu", "achieved": achieved_ops / 1e12,
                          "peak": peak_ops / 1e12, "unit": "Tops/s",
