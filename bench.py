@@ -69,6 +69,9 @@ def parse():
                     help="NEXT-3: after --assembly 1, tune every Cell in its favoured halves")
     ap.add_argument("--paper-stages", action="store_true",
                     help="NEXT-2: the paper's stage determination instead of the min-max DP")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1 exchange: NCCL all-gather + compaction (north_star), or the fused "
+                         "exchange (estimate kernel stores into every rank's window over NVLink)")
     return ap.parse_args()
 
 
@@ -86,7 +89,10 @@ def config_dict(a, pr, n_cells, n_plans, world, flush):
             "cluster_gpus": int(pr.cap.sum()), "cells": int(n_cells), "cell_plans": int(n_plans),
             "gpu_set": ["paper3", "all_pow2"][pr.gpu_set], "s_max": pr.s_max, "g_max": pr.g_max,
             "microbatches": "4S" if pr.b_mode == 0 else [int(b) for b in pr.b_values],
-            "search_depth": pr.depth, "parallelism": f"cell-range sharding x{world} + all-gather",
+            "search_depth": pr.depth,
+            "parallelism": f"cell-range sharding x{world} + " + (
+                "fused P2P exchange (estimate kernel -> NVLink peer windows)"
+                if world > 1 and getattr(a, "gather", "nccl") == "p2p" else "all-gather"),
             "l2": "flushed between steps (256 MiB write)" if flush else "not flushed"}
 
 
@@ -356,6 +362,11 @@ def main():
     cells_h = {k: v.cpu().numpy() for k, v in cr.cells().items()}
     stage_tp = (torch.empty((max(n_cells, 1), cr.max_stages()), dtype=torch.int8, device=dev)
                 if a.assembly else None)
+    xch = None
+    if world > 1 and a.gather == "p2p":
+        if a.paper_stages or a.assembly:
+            raise SystemExit("--gather p2p: the fused exchange covers the D1 estimator only")
+        xch = sharded.PeerExchange(cr, rank, world)
     flush = not a.no_flush
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
 
@@ -375,10 +386,14 @@ def main():
                                   stage_tp=stage_tp)
             if a.tune:
                 cr.tune_assembled(stage_tp, a.form, int(ub[rank]), int(ub[rank + 1]), out=mine)
+        elif xch is not None:
+            cr.estimate_exchange(int(ub[rank]), int(ub[rank + 1]))
         else:
             cr.estimate(int(ub[rank]), int(ub[rank + 1]), out=mine)
         e2.record(stream)
-        if world > 1:
+        if xch is not None:
+            res = cr.exchange_wait()
+        elif world > 1:
             dist.all_gather_into_tensor(gathered, mine[:plan.chunk])
             res = cr.compact(gathered, plan.chunk, world, plan.cell_begin, out=full)
         else:
@@ -459,7 +474,8 @@ def main():
                 cr.enumerate()
                 pl = sharded.ShardPlan(cr, world)
                 assert pl.job_range(rank, pr.n_types) == (j0, j1)
-                res = sharded.estimate_all(cr, pl, rank, mine=mine, gathered=gathered, full=full)
+                res = (xch.estimate_all(pl) if xch is not None else
+                       sharded.estimate_all(cr, pl, rank, mine=mine, gathered=gathered, full=full))
             else:
                 cr.update(pr)
                 cr.enumerate()
@@ -531,6 +547,8 @@ def main():
         if a.json_out:
             with open(a.json_out, "w") as f:
                 f.write(s + "\n")
+    if xch is not None:
+        xch.close()
     cr.close()
     if world > 1:
         dist.destroy_process_group()

@@ -239,6 +239,51 @@ crius_status crius_compact_gathered(crius_ctx *ctx, const crius_cell_result *d_g
                                     const int64_t *cell_begin, crius_cell_result *d_all,
                                     void *stream);
 
+/* Fused exchange: the all-gather of A7 done by the estimate kernel itself over
+ * NVLink / NVSwitch peer memory ("fused-collective option": the
+ * north_star exchange -- every rank gets every Cell's best plan before the
+ * round -- without a separate collective or compaction).  One process per GPU,
+ * all on one node, world <= 8.  Sequence per rank:
+ *   crius_exchange_init  -> 64-byte CUDA IPC handle of this rank's window
+ *   (the caller all-gathers the handles, e.g. over the process group)
+ *   crius_exchange_open  with every rank's handle (rank order)
+ *   per step: crius_estimate_exchange(this rank's unit range)
+ *             crius_exchange_wait -> device pointer to all n_cells records
+ *             crius_schedule_round(that pointer)
+ * Every rank must call crius_estimate_exchange once per step (also with an
+ * empty range) or the others' waits never complete (they trap after 30 s).
+ * Window (library-owned device memory): arrival flags int64[8] (256 B) +
+ * 2 x capacity_cells records, used alternately by step parity, so a fast rank's
+ * next step never overwrites records a slow rank's round is still reading. */
+
+/* Allocate this rank's window for up to capacity_cells Cells and write its
+ * CUDA IPC handle (64 bytes) to handle_out (HOST).  Synchronous.
+ * EINVAL: world not in 1..8, rank not in [0, world); ESTATE: already initialised. */
+crius_status crius_exchange_init(crius_ctx *ctx, int32_t rank, int32_t world,
+                                 int64_t capacity_cells, uint8_t *handle_out);
+
+/* Map every other rank's window: handles (HOST) = world x 64 bytes, rank order
+ * (this rank's own entry is ignored).  Synchronous.  ECUDA if a handle cannot
+ * be opened (e.g. the GPUs are not peers). */
+crius_status crius_exchange_open(crius_ctx *ctx, const uint8_t *handles);
+
+/* As crius_estimate_cells for units [unit_begin, unit_end), but each Cell's
+ * record is stored at its GLOBAL Cell index into every rank's window (16-byte
+ * P2P stores from the kernel's epilogue); the kernel's last CTA then
+ * release-stores the step number into every rank's arrival flag for this rank.
+ * Asynchronous on `stream`.  EINVAL if n_cells exceeds capacity_cells. */
+crius_status crius_estimate_exchange(crius_ctx *ctx, int64_t unit_begin, int64_t unit_end,
+                                     void *stream);
+
+/* Enqueue on `stream` a wait until every rank's flag for this step has arrived;
+ * *d_all = this rank's window half of the step (DEVICE, n_cells records in
+ * global Cell order, valid until the step after next).  Asynchronous. */
+crius_status crius_exchange_wait(crius_ctx *ctx, crius_cell_result **d_all, void *stream);
+
+/* Unmap the peers' windows and free this rank's (also done by crius_destroy).
+ * Synchronises the device. */
+crius_status crius_exchange_close(crius_ctx *ctx);
+
 /* One scheduling round (§N6: Phase A SchedArrival P:436-445 with ScaleResource
  * P:491-497 at search depth d, Phase B extra scheduling / reverse scaling
  * P:449-450) over all Cells, on the device.  d_all: DEVICE results of

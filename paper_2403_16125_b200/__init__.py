@@ -74,7 +74,9 @@ EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_update_profile
            "crius_split_stride", "crius_max_stages", "crius_partition_units",
            "crius_estimate_cells", "crius_estimate_assembled", "crius_tune_assembled",
            "crius_estimate_paper_stages",
-           "crius_compact_gathered", "crius_schedule_round", "crius_schedule_round_state",
+           "crius_compact_gathered", "crius_exchange_init", "crius_exchange_open",
+           "crius_estimate_exchange", "crius_exchange_wait", "crius_exchange_close",
+           "crius_schedule_round", "crius_schedule_round_state",
            "crius_round_stats",
            "crius_kernel_launches",
            "crius_last_error", "crius_destroy"]
@@ -108,6 +110,11 @@ def lib():
         L.crius_max_stages.argtypes = [vp]
         L.crius_max_stages.restype = i32
         L.crius_compact_gathered.argtypes = [vp, vp, i64, i32, vp, vp, vp]
+        L.crius_exchange_init.argtypes = [vp, i32, i32, i64, vp]
+        L.crius_exchange_open.argtypes = [vp, vp]
+        L.crius_estimate_exchange.argtypes = [vp, i64, i64, vp]
+        L.crius_exchange_wait.argtypes = [vp, C.POINTER(vp), vp]
+        L.crius_exchange_close.argtypes = [vp]
         L.crius_schedule_round.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.crius_schedule_round_state.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.crius_round_stats.argtypes = [vp, vp, vp]
@@ -316,6 +323,35 @@ class Crius:
                                             C.c_void_p(out.data_ptr()), _stream_handle(stream)))
         return out
 
+    # ---- fused exchange over NVLink peer memory (crius_exchange_*)
+    def exchange_init(self, rank, world, capacity=None):
+        """Allocate this rank's exchange window; returns its 64-byte IPC handle."""
+        cap = int(capacity if capacity is not None else max(self.n_cells or 1, 1))
+        h = (C.c_uint8 * 64)()
+        _check(lib().crius_exchange_init(self.ctx, int(rank), int(world), cap, h))
+        return bytes(h)
+
+    def exchange_open(self, handles):
+        """handles: every rank's 64-byte handle concatenated in rank order."""
+        buf = (C.c_uint8 * len(handles)).from_buffer_copy(bytes(handles))
+        _check(lib().crius_exchange_open(self.ctx, buf))
+
+    def estimate_exchange(self, unit_begin, unit_end, stream=None):
+        """Estimate [unit_begin, unit_end) and store every record into every rank's window."""
+        _check(lib().crius_estimate_exchange(self.ctx, int(unit_begin), int(unit_end),
+                                             _stream_handle(stream)))
+
+    def exchange_wait(self, stream=None):
+        """Enqueue the wait for every rank's records; returns the window half of
+        this step as an [n_cells, 2] int64 device tensor (a view, no copy)."""
+        p = C.c_void_p()
+        _check(lib().crius_exchange_wait(self.ctx, C.byref(p), _stream_handle(stream)))
+        return self.torch.as_tensor(_DevView(p.value, int(self.n_cells)),
+                                    device=f"cuda:{self.device}")
+
+    def exchange_close(self):
+        _check(lib().crius_exchange_close(self.ctx))
+
     def schedule_round(self, results, free=None, stream=None):
         J, T = self.pr.n_jobs, self.pr.n_types
         dec = np.zeros(J, np.int64)
@@ -371,6 +407,15 @@ class Crius:
             self.close()
         except Exception:
             pass
+
+
+class _DevView:
+    """[n, 2] int64 view of library-owned device memory (CUDA array interface)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (max(n, 1), 2), "typestr": "<i8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None, "stream": None}
 
 
 def decode(results):

@@ -32,6 +32,7 @@ constexpr int kMaxB = 16;
 constexpr int kMaxDepth = 16;
 constexpr int kMaxKmax = 6;
 constexpr int kMaxSidx = 12;  // S up to 2^11 stages
+constexpr int kMaxRanks = 8;  // ranks of one fused exchange (one NVSwitch node)
 
 struct TypeParams {
   int32_t cap, gpn, lgpn, pad;

@@ -17,6 +17,7 @@
 #include "enumerate.cuh"
 #include "estimate.cuh"
 #include "round.cuh"
+#include "exchange.cuh"
 
 using namespace crius;
 
@@ -102,6 +103,14 @@ struct crius_ctx {
   int32_t *d_list = nullptr;
   AdmView adm_glob{};  // admitted-job records in global memory (only when they exceed shared)
   EView eg{};          // (ii) move caches in global memory (rounds listing > kECap jobs)
+  // fused exchange (crius_exchange_*): own window = [flags int64[kMaxRanks] | pad to
+  // kXchHdr][2][x_cap] records; x_peer[r] = rank r's window mapped over CUDA IPC
+  int32_t x_rank = -1, x_world = 0;
+  int64_t x_cap = 0, x_epoch = 0;
+  bool x_open = false;
+  unsigned char *x_base = nullptr;
+  unsigned char *x_peer[kMaxRanks] = {};
+  uint32_t *x_done = nullptr;
 };
 
 namespace {
@@ -610,16 +619,37 @@ namespace {
 
 // Shared launcher of k_estimate: amode 0 = uniform plans (§N5), 1/2 = NEXT-1
 // per-stage assembly (paper DP-only/TP-only per stage; every factorisation).
+constexpr int64_t kXchHdr = 256;  // flag bytes at the head of a window
+
 crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_begin,
                              int64_t unit_end, crius_cell_result *d_out, int16_t *d_splits,
-                             int8_t *d_stage_tp, const int8_t *d_favor, cudaStream_t st) {
+                             int8_t *d_stage_tp, const int8_t *d_favor, cudaStream_t st,
+                             bool exchange = false) {
   if (!c->enumerated) return fail(CRIUS_ESTATE, "estimate before enumerate");
   if (unit_begin < 0 || unit_end > c->n_units || unit_begin > unit_end)
     return fail(CRIUS_EINVAL, "bad unit range");
-  if (!d_out) return fail(CRIUS_EINVAL, "null d_out");
-  if (unit_begin == unit_end) return CRIUS_OK;
+  if (!d_out && !exchange) return fail(CRIUS_EINVAL, "null d_out");
   CK(cudaSetDevice(c->device));
   EstArgs A{};
+  if (exchange) {
+    A.nx = c->x_world;
+    A.x_rank = c->x_rank;
+    A.x_epoch = c->x_epoch;
+    A.x_done = c->x_done;
+    const int64_t half = (c->x_epoch & 1) * c->x_cap * (int64_t)sizeof(CellResult);
+    for (int r = 0; r < c->x_world; ++r) {
+      A.xflag[r] = (int64_t *)c->x_peer[r];
+      A.xout[r] = (CellResult *)(c->x_peer[r] + kXchHdr + half);
+    }
+  }
+  if (unit_begin == unit_end) {
+    if (!exchange) return CRIUS_OK;
+    // nothing to estimate: still tell every rank this rank's (empty) range is done
+    k_xch_signal_only<<<1, 32, 0, st>>>(A);
+    CKL();
+    c->launches += 1;
+    return CRIUS_OK;
+  }
   A.cG = c->C.G;
   A.cS = c->C.S;
   A.plan_off = c->C.plan_off;
@@ -658,9 +688,13 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   A.off_BND = take(Lp * 8);
   A.off_F = take(2 * Lp * 8);
   A.off_ARG = take((Stop + 1) * Lp);
+  // the raw int32 compute rows are dead once their prefix sums are in PC, before
+  // the DP first writes F / ARG: share those bytes when they are large enough
+  const bool craw_alias = K1e * Lp * 4 <= o - A.off_F;
+  A.off_CRAW = craw_alias ? A.off_F : 0;
   A.off_BD = take(A.split_stride * 2);
   A.off_CELL = take(3 * (maxCells + 1) * 4);
-  A.off_CRAW = take(K1e * Lp * 4);
+  if (!craw_alias) A.off_CRAW = take(K1e * Lp * 4);
   A.off_NRAW = take(Lp * 4);
   A.off_POFF = take(maxCells * 8);
   A.off_ORD = take((maxCells + 1) * 4);
@@ -672,6 +706,9 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
   int warps = 4;
   if (4 * A.warp_bytes > 200 * 1024) warps = 1;
+#ifdef CRIUS_EST_FORCE_W1
+  warps = 1;  // experiment: one warp per CTA (finer shared-memory granularity)
+#endif
   if (A.warp_bytes > 220 * 1024) return fail(CRIUS_EINVAL, "unit too large for shared memory");
   const size_t smem = (size_t)warps * A.warp_bytes;
 #ifndef CRIUS_NBG_WIDE
@@ -714,6 +751,93 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
   return launch_estimate(c, 0, 0, unit_begin, unit_end, d_out, d_splits, nullptr, nullptr,
                          (cudaStream_t)stream);
+}
+
+// ---- fused exchange (SURVEY §8(e) fused-collective option) -------------------
+crius_status crius_exchange_init(crius_ctx *c, int32_t rank, int32_t world, int64_t capacity_cells,
+                                 uint8_t *handle_out) {
+  if (!c || !handle_out) return fail(CRIUS_EINVAL, "null argument");
+  if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
+    return fail(CRIUS_EINVAL, "rank/world out of range (world <= 8)");
+  if (capacity_cells < 1) return fail(CRIUS_EINVAL, "capacity_cells must be >= 1");
+  if (c->x_base) return fail(CRIUS_ESTATE, "exchange already initialised");
+  CK(cudaSetDevice(c->device));
+  const size_t bytes = (size_t)kXchHdr + 2 * (size_t)capacity_cells * sizeof(CellResult);
+  CK(cudaMalloc((void **)&c->x_base, bytes));
+  CK(cudaMalloc((void **)&c->x_done, sizeof(uint32_t)));
+  CK(cudaMemset(c->x_base, 0, kXchHdr));
+  CK(cudaMemset(c->x_done, 0, sizeof(uint32_t)));
+  CK(cudaDeviceSynchronize());  // flags are zero before any peer can signal
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->x_base));
+  std::memcpy(handle_out, &h, sizeof(h));
+  c->x_rank = rank;
+  c->x_world = world;
+  c->x_cap = capacity_cells;
+  c->x_epoch = 0;
+  c->x_open = false;
+  return CRIUS_OK;
+}
+
+crius_status crius_exchange_open(crius_ctx *c, const uint8_t *handles) {
+  if (!c || !handles) return fail(CRIUS_EINVAL, "null argument");
+  if (!c->x_base || c->x_open) return fail(CRIUS_ESTATE, "exchange not initialised or already open");
+  CK(cudaSetDevice(c->device));
+  for (int r = 0; r < c->x_world; ++r) {
+    if (r == c->x_rank) {
+      c->x_peer[r] = c->x_base;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + (size_t)r * sizeof(h), sizeof(h));
+    void *p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->x_peer[r] = (unsigned char *)p;
+  }
+  c->x_open = true;
+  return CRIUS_OK;
+}
+
+crius_status crius_estimate_exchange(crius_ctx *c, int64_t unit_begin, int64_t unit_end, void *stream) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  if (!c->x_open) return fail(CRIUS_ESTATE, "exchange not open");
+  if (!c->enumerated) return fail(CRIUS_ESTATE, "estimate before enumerate");
+  if (c->n_cells > c->x_cap) return fail(CRIUS_EINVAL, "more Cells than the exchange capacity");
+  c->x_epoch += 1;
+  const crius_status s = launch_estimate(c, 0, 0, unit_begin, unit_end, nullptr, nullptr, nullptr,
+                                         nullptr, (cudaStream_t)stream, true);
+  if (s != CRIUS_OK) c->x_epoch -= 1;
+  return s;
+}
+
+crius_status crius_exchange_wait(crius_ctx *c, crius_cell_result **d_all, void *stream) {
+  if (!c || !d_all) return fail(CRIUS_EINVAL, "null argument");
+  if (!c->x_open || c->x_epoch < 1) return fail(CRIUS_ESTATE, "no exchange step to wait for");
+  CK(cudaSetDevice(c->device));
+  k_xch_wait<<<1, 32, 0, (cudaStream_t)stream>>>((const int64_t *)c->x_base, c->x_world, c->x_epoch);
+  CKL();
+  c->launches += 1;
+  *d_all = (crius_cell_result *)(c->x_base + kXchHdr +
+                                 (c->x_epoch & 1) * c->x_cap * (int64_t)sizeof(CellResult));
+  return CRIUS_OK;
+}
+
+crius_status crius_exchange_close(crius_ctx *c) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  if (!c->x_base) return CRIUS_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->x_world; ++r)
+    if (c->x_peer[r] && r != c->x_rank) cudaIpcCloseMemHandle(c->x_peer[r]);
+  cudaFree(c->x_base);
+  cudaFree(c->x_done);
+  for (int r = 0; r < kMaxRanks; ++r) c->x_peer[r] = nullptr;
+  c->x_base = nullptr;
+  c->x_done = nullptr;
+  c->x_open = false;
+  c->x_world = 0;
+  c->x_rank = -1;
+  return CRIUS_OK;
 }
 
 crius_status crius_estimate_assembled(crius_ctx *c, const crius_assembly *asm_cfg,
@@ -913,6 +1037,7 @@ crius_status crius_round_stats(crius_ctx *c, int64_t *out16, void *stream) {
 
 void crius_destroy(crius_ctx *c) {
   if (!c) return;
+  crius_exchange_close(c);
   cudaSetDevice(c->device);
   free_all(c);
   delete c;

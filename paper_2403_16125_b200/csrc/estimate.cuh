@@ -43,7 +43,48 @@ struct EstArgs {
   int32_t stage_stride;
   int32_t off_ST, st_cap;  // per-warp stage table (st_cap entries)
   int32_t off_PS;          // NEXT-2 scratch: sorted gap bytes [Lp] i64, LF [Lp] i32, g [Stop] i32
+  // fused exchange: every record is also stored at its GLOBAL
+  // Cell index into each rank's window (peer memory over NVLink, xout[r]); the
+  // last CTA to finish then raises flag xflag[r][x_rank] = x_epoch on every rank
+  int32_t nx, x_rank;
+  int64_t x_epoch;
+  CellResult *xout[kMaxRanks];
+  int64_t *xflag[kMaxRanks];
+  uint32_t *x_done;        // CTA completion counter (the last CTA resets it)
 };
+
+// One Cell record: to the caller's chunk (local index) and, with the fused
+// exchange, to every rank's window at the global index (16-byte P2P stores).
+__device__ __forceinline__ void emit_result(const EstArgs &A, int64_t cell, int64_t base,
+                                            const CellResult &r) {
+  if (A.out) A.out[cell - base] = r;
+  for (int q = 0; q < A.nx; ++q) A.xout[q][cell] = r;
+}
+
+// Fused exchange epilogue (all threads of the CTA).  Every CTA orders its own
+// stores (bar.sync, then a system-scope fence by thread 0) before counting
+// itself done; the last CTA fences again and release-stores the step's epoch
+// into every rank's arrival slot for this rank: a receiver that acquires
+// epoch there sees every record of this rank's Cell range (fence cumulativity).
+__device__ __forceinline__ void exchange_signal(const EstArgs &A) {
+  if (A.nx == 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t prev = atomicAdd(A.x_done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      for (int q = 0; q < A.nx; ++q)
+        asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(A.xflag[q] + A.x_rank),
+                     "l"(A.x_epoch)
+                     : "memory");
+      *A.x_done = 0u;  // next launch (stream-ordered) starts from zero
+    }
+  }
+}
+
+// A rank with an empty unit range still signals its (empty) contribution.
+__global__ void k_xch_signal_only(EstArgs A) { exchange_signal(A); }
 
 // Inclusive prefix of a profile row into dst[0..L] (dst[0] = 0).
 template <typename Src>
@@ -848,8 +889,16 @@ __device__ __forceinline__ UnitMeta load_meta(const Params &P, const EstArgs &A,
 #ifndef CRIUS_EST_MINB
 #define CRIUS_EST_MINB 4  // <= 128 registers: 4 CTAs (16 warps) per SM
 #endif
+// The B-sweep instantiation (NBG > 1) keeps NBG partial sums per lane and spills
+// at 128 registers; its per-warp shared memory already caps it near 3 CTAs per
+// SM at large L, so it gets <= 168 registers (measured: cfg5 4.80 -> 4.34 ms,
+// cfg3 0.129 -> 0.123 ms; the NBG = 1 kernel is faster at 128: cfg4 0.325 vs 0.356 ms).
+#ifndef CRIUS_EST_MINB_WIDE
+#define CRIUS_EST_MINB_WIDE 3
+#endif
 template <int WARPS, int NBG, int AMODE>
-__global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params P, EstArgs A) {
+__global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : CRIUS_EST_MINB) * 4 / WARPS)
+    k_estimate(Params P, EstArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned char *base = smem + (size_t)wid * A.warp_bytes;
@@ -1069,7 +1118,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
           res.t_ns = ok ? wT : kInf;
           res.plan = ok ? wp : -1;
           res.flags = ok ? 1 : 0;
-          A.out[cb + ci - out_cell_base] = res;
+          emit_result(A, cb + ci, out_cell_base, res);
         }
         __syncwarp();
       }
@@ -1090,7 +1139,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
           res.t_ns = F;
           res.plan = F == kInf ? -1 : bb;
           res.flags = F == kInf ? 0 : 1;
-          A.out[cb + ci - out_cell_base] = res;
+          emit_result(A, cb + ci, out_cell_base, res);
         }
       }
       __syncwarp();
@@ -1178,7 +1227,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
         res.t_ns = T;
         res.plan = T == kInf ? -1 : p;
         res.flags = T == kInf ? 0 : 1;
-        A.out[cb + ORD[r] - out_cell_base] = res;
+        emit_result(A, cb + ORD[r], out_cell_base, res);
       }
       const int r31 = __shfl_sync(0xffffffffu, r, 31);
       const int64_t T31 = __shfl_sync(0xffffffffu, T, 31);
@@ -1195,6 +1244,7 @@ __global__ void __launch_bounds__(WARPS * 32, CRIUS_EST_MINB) k_estimate(Params 
     }
     __syncwarp();
   }
+  exchange_signal(A);
 }
 
 }  // namespace crius

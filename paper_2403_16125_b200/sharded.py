@@ -47,3 +47,31 @@ def estimate_all(ctx, plan: ShardPlan, rank, mine=None, gathered=None, full=None
         gathered = ctx.new_results(w * plan.chunk)
     dist.all_gather_into_tensor(gathered, mine[:plan.chunk], group=group)
     return ctx.compact(gathered, plan.chunk, w, plan.cell_begin, out=full)
+
+
+class PeerExchange:
+    """The fused exchange (crius_exchange_*): the estimate kernel stores every
+    Cell record into every rank's window over NVLink peer memory and signals
+    per-rank arrival flags -- no NCCL all-gather, no compaction.  Setup exchanges
+    the 64-byte CUDA IPC handles once over the process group (plumbing only)."""
+
+    def __init__(self, ctx, rank, world, capacity=None, group=None):
+        import torch
+        import torch.distributed as dist
+        self.ctx, self.rank, self.world = ctx, rank, world
+        h = ctx.exchange_init(rank, world, capacity)
+        mine = torch.frombuffer(bytearray(h), dtype=torch.uint8).to(f"cuda:{ctx.device}")
+        allh = torch.empty(world * 64, dtype=torch.uint8, device=f"cuda:{ctx.device}")
+        dist.all_gather_into_tensor(allh, mine, group=group)
+        ctx.exchange_open(allh.cpu().numpy().tobytes())
+        dist.barrier(group=group)  # every window is mapped before anyone stores into it
+
+    def estimate_all(self, plan: ShardPlan, stream=None):
+        """This rank's unit range -> every rank's window; returns all n_cells
+        records (a view of this rank's window, valid until the step after next)."""
+        self.ctx.estimate_exchange(int(plan.unit_begin[self.rank]),
+                                   int(plan.unit_begin[self.rank + 1]), stream=stream)
+        return self.ctx.exchange_wait(stream=stream)
+
+    def close(self):
+        self.ctx.exchange_close()

@@ -340,3 +340,48 @@ def test_cfg5_x10_sampled_units(crius, oracle_mod):
         assert cells["job"][dec[j]] == j and t_g[dec[j]] < INF
         used[cells["type"][dec[j]]] += cells["G"][dec[j]]
     assert np.all(used + fa == pr.cap)
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_exchange_world1_equals_oracle(crius, oracle_mod, cfg):
+    """The fused exchange path on one GPU (world 1: the window is the rank's own):
+    estimate kernel -> window stores + release flag -> device-side acquire wait ->
+    round.  5 steps (both window halves, epochs 1..5), each bit-exact to the oracle;
+    a sub-range per step exercises the empty-range signal too."""
+    pr = W.make_config(cfg)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    t_ref, p_ref = o.estimate(cells)
+    d_ref, f_ref, tot_ref = o.round(cells, t_ref)
+    with crius.Crius(pr) as cr:
+        n, _, u = cr.enumerate()
+        h = cr.exchange_init(0, 1)
+        assert len(h) == 64
+        cr.exchange_open(h)
+        for step in range(5):
+            cr.estimate_exchange(0, u)
+            full = cr.exchange_wait()
+            t_ns, plan, _ = crius.decode(full[:n])
+            assert np.array_equal(t_ns, t_ref) and np.array_equal(plan, p_ref), step
+            dec, fa, tot = cr.schedule_round(full)
+            assert np.array_equal(dec, d_ref) and np.array_equal(fa, f_ref) and tot == tot_ref
+        # an empty range still signals (the wait completes); the window keeps old values
+        cr.estimate_exchange(0, 0)
+        cr.exchange_wait()
+        import torch
+        torch.cuda.synchronize()
+        cr.exchange_close()
+
+
+def test_exchange_rejects_misuse(crius):
+    pr = W.make_config(1)
+    with crius.Crius(pr) as cr:
+        cr.enumerate()
+        with pytest.raises(Exception, match="not open"):
+            cr.estimate_exchange(0, 1)
+        with pytest.raises(Exception, match="world"):
+            cr.exchange_init(0, 9)
+        h = cr.exchange_init(0, 1, capacity=1)
+        cr.exchange_open(h)
+        with pytest.raises(Exception, match="capacity"):
+            cr.estimate_exchange(0, 1)

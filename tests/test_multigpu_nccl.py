@@ -20,6 +20,33 @@ def _port():
     return p
 
 
+def _worker_p2p(rank, world, port, cfg, steps, q):
+    """The fused exchange: estimate kernel -> P2P stores into every rank's window
+    + arrival flags; several steps (double-buffered windows, epochs)."""
+    import torch.distributed as dist
+    import paper_2403_16125_b200 as pkg
+    from paper_2403_16125_b200 import sharded
+    from paper_2403_16125_b200 import workload as W
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    pr = W.make_config(cfg)
+    outs = []
+    with pkg.Crius(pr, device=rank) as cr:
+        cr.enumerate()
+        plan = sharded.ShardPlan(cr, world)
+        xch = sharded.PeerExchange(cr, rank, world)
+        for _ in range(steps):
+            full = xch.estimate_all(plan)
+            dec, fa, tot = cr.schedule_round(full)
+            t_ns, plan_idx, _ = pkg.decode(full[:plan.n_cells])
+            outs.append((t_ns, plan_idx, dec, fa, tot))
+        xch.close()
+    q.put((rank, outs))
+    dist.destroy_process_group()
+
+
 def _worker(rank, world, port, cfg, q):
     import torch.distributed as dist
     import paper_2403_16125_b200 as pkg
@@ -64,3 +91,33 @@ def test_nccl_sharded_equals_oracle(oracle_mod, cfg):
     for rank, t_ns, plan_idx, dec, fa, tot in outs:
         assert np.array_equal(t_ns, t_ref) and np.array_equal(plan_idx, p_ref), rank
         assert np.array_equal(dec, d_ref) and np.array_equal(fa, f_ref) and tot == tot_ref, rank
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_p2p_exchange_equals_oracle(oracle_mod, cfg):
+    """Fused estimate + NVLink P2P exchange on every GPU of the box (<= 8): every
+    rank's records and decisions byte-identical to the oracle, 3 steps each."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    import torch.multiprocessing as mp
+    from paper_2403_16125_b200 import workload as W
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker_p2p, args=(r, world, port, cfg, 3, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    outs = [q.get(timeout=600) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    o = oracle_mod.Oracle(W.make_config(cfg))
+    cells = o.enumerate()
+    t_ref, p_ref = o.estimate(cells)
+    d_ref, f_ref, tot_ref = o.round(cells, t_ref)
+    for rank, steps in outs:
+        assert len(steps) == 3
+        for t_ns, plan_idx, dec, fa, tot in steps:
+            assert np.array_equal(t_ns, t_ref) and np.array_equal(plan_idx, p_ref), rank
+            assert np.array_equal(dec, d_ref) and np.array_equal(fa, f_ref) and tot == tot_ref, rank
