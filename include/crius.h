@@ -310,6 +310,26 @@ crius_status crius_schedule_round_state(crius_ctx *ctx, const crius_cell_result 
                                         const uint8_t *active, int64_t *decision,
                                         int32_t *free_after, double *total_score, void *stream);
 
+/* NEXT-4 ablations of the round (Fig. `ablation`; reading
+ * R-11 in DESIGN.md): policy bit 0 = NA, no adaptivity scaling -- every job's
+ * options are restricted to G = N_G, so no GPU count ever changes; bit 1 = NH,
+ * no heterogeneity scaling -- an admitted job never changes its GPU type (no
+ * other-type victim move in ScaleResource, Phase B only within the type; a
+ * job's first placement may use any type).  0 = the full round (default).
+ * Applies to every later crius_schedule_round(_state) call of this context.
+ * EINVAL unless 0 <= policy <= 3. */
+crius_status crius_set_round_policy(crius_ctx *ctx, int32_t policy);
+
+/* Deadline-aware rounds ("strict deadline guarantees for
+ * each scheduled job"; reading R-12 in DESIGN.md).  t_max (HOST int64
+ * [n_jobs], read during the call; NULL = no deadlines): per job, the largest
+ * iteration time an option may have (the caller derives it from the deadline,
+ * the remaining iterations and any restart penalty); a Cell with T > t_max[j]
+ * is not an option of job j, except the (type, G) a running job uses.  Applies
+ * to every later round of this context until reset with NULL.  Asynchronous
+ * upload on `stream`. */
+crius_status crius_set_deadline_bounds(crius_ctx *ctx, const int64_t *t_max, void *stream);
+
 /* Counters of the last round (HOST out16[21]): [0] speculative Phase A batches,
  * [1] victim-sequence recomputations, [2] SM cycles in them, [3] SM cycles of
  * Phase A, [4] SM cycles of Phase B, [5] admitted jobs, [6] admissions through

@@ -204,7 +204,10 @@ class Oracle:
             "estimate_paper")
         return t_ns, plan, lg.reshape(c1 - c0, kstride)
 
-    def round_state(self, cells, t_ns, free_in, run_cell=None, active=None):
+    def round_state(self, cells, t_ns, free_in, run_cell=None, active=None, policy=0,
+                    t_max=None):
+        """NEXT-4 round from a state; policy bit 0 = NA, bit 1 = NH (ablations, R-11);
+        t_max: per-job deadline bound on an option's T (R-12), None = no deadlines."""
         J, T = self.pr.n_jobs, self.pr.n_types
         dec = np.zeros(J, np.int64)
         fa = np.zeros(T, np.int32)
@@ -212,10 +215,13 @@ class Oracle:
         fi = np.ascontiguousarray(free_in, np.int32)
         rc, rcp = _opt_ptr(run_cell, np.int64)
         ac, acp = _opt_ptr(active, np.uint8)
+        tm, tmp = _opt_ptr(t_max, np.int64)
         t_ns = np.ascontiguousarray(t_ns, np.int64)
-        self._check(self.L.oracle_round_state(
+        self._check(self.L.oracle_round_policy(
             C.byref(self.s), C.c_int64(len(t_ns)), *[_ptr(cells[k]) for k in ("job", "type", "G", "S")],
-            _ptr(t_ns), _ptr(fi), rcp, acp, _ptr(dec), _ptr(fa), C.byref(tot)), "round_state")
+            _ptr(t_ns), _ptr(fi), rcp, acp, C.c_int32(policy), tmp, _ptr(dec), _ptr(fa),
+            C.byref(tot)),
+            "round_state")
         return dec, fa, tot.value
 
     def round(self, cells, t_ns, free_in=None):

@@ -805,7 +805,29 @@ int oracle_round_state(const oracle_problem *pr, int64_t n_cells, const int32_t 
                        const int64_t *t_ns, const int32_t *free_in, const int64_t *run_cell,
                        const uint8_t *active, int64_t *decision, int32_t *free_after,
                        double *total_score) {
-  if (!valid_problem(pr) || n_cells < 0) return 2;
+  return oracle_round_policy(pr, n_cells, cell_job, cell_type, cell_G, cell_S, t_ns, free_in,
+                             run_cell, active, 0, nullptr, decision, free_after, total_score);
+}
+
+/* NEXT-4 ablations ("adaptivity scaling as changing the
+ * allocated number of GPUs, heterogeneity scaling as changing the allocated GPU
+ * type"), reading R-11: policy bit 0 (NA) keeps every job at its requested N_G
+ * -- O_j holds only the options with G = N_G (ref_j is unchanged); bit 1 (NH)
+ * keeps every admitted job on its GPU type -- no other-type victim move (case
+ * ii) and Phase B only considers options of the job's current type; a job's
+ * first placement may use any type.
+ * Deadline-aware variant ("strict deadline guarantees for
+ * each scheduled job"), reading R-12: t_max (per job, NULL = none) bounds the
+ * iteration time of the job's options -- a Cell with T > t_max[j] is not an
+ * option, except the (type, G) a running job currently uses (its completion
+ * was guaranteed when it was placed). */
+int oracle_round_policy(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,
+                        const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                        const int64_t *t_ns, const int32_t *free_in, const int64_t *run_cell,
+                        const uint8_t *active, int32_t policy, const int64_t *t_max,
+                        int64_t *decision, int32_t *free_after, double *total_score) {
+  if (!valid_problem(pr) || n_cells < 0 || policy < 0 || policy > 3) return 2;
+  const bool no_adapt = (policy & 1) != 0, no_hetero = (policy & 2) != 0;
   const int32_t J = pr->n_jobs, TT = pr->n_types, d = pr->depth;
 
   // Options O_j: for each (t, G) with a feasible Cell, the Cell with min (T_c, S_c),
@@ -823,6 +845,12 @@ int oracle_round_state(const oracle_problem *pr, int64_t n_cells, const int32_t 
     if (t_ns[c] == INF) continue;
     ref_any[j] = std::min(ref_any[j], t_ns[c]);
     if (cell_G[c] == pr->ng[j]) ref[j] = std::min(ref[j], t_ns[c]);
+    if (no_adapt && cell_G[c] != pr->ng[j]) continue;  // NA: only G = N_G is an option
+    if (t_max && t_ns[c] > t_max[j]) {  // deadline: too slow, unless the running (type, G)
+      const bool running = run_cell && run_cell[j] >= 0 && (active == nullptr || active[j] != 0);
+      if (!running || cell_type[c] != cell_type[run_cell[j]] || cell_G[c] != cell_G[run_cell[j]])
+        continue;
+    }
     bool found = false;
     for (Opt &o : O[j])
       if (o.t == cell_type[c] && o.G == cell_G[c]) {
@@ -899,7 +927,7 @@ int oracle_round_state(const oracle_problem *pr, int64_t n_cells, const int32_t 
             if (o2.t == o.t && o2.G < cv.G) {
               freed = cv.G - o2.G;
               other = false;
-            } else if (o2.t != o.t && o2.G <= fr2[o2.t]) {
+            } else if (!no_hetero && o2.t != o.t && o2.G <= fr2[o2.t]) {
               freed = cv.G;
               other = true;
             } else {
@@ -963,6 +991,7 @@ int oracle_round_state(const oracle_problem *pr, int64_t n_cells, const int32_t 
       for (int32_t i = 0; i < (int32_t)O[j].size(); ++i) {
         if (i == cur[j]) continue;
         const Opt &o = O[j][i];
+        if (no_hetero && o.t != cj.t) continue;  // NH: an admitted job keeps its type
         const int32_t avail = fr[o.t] + (o.t == cj.t ? cj.G : 0);
         if (o.G <= avail && o.T < cj.T && (best < 0 || kappa_less(o, O[j][best]))) best = i;
       }

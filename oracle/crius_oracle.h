@@ -108,6 +108,14 @@ int oracle_round(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_
 
 /* NEXT-4: the round from a cluster state (running jobs start admitted on
  * the option of their Cell's (type, G); inactive jobs get decision -3). */
+/* NEXT-4 ablations: as oracle_round_state with policy bit 0 = NA (options only
+ * at G = N_G), bit 1 = NH (admitted jobs keep their GPU type); t_max (per job
+ * or NULL): deadline bound on an option's T (a running job's (type, G) exempt). */
+int oracle_round_policy(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,
+                        const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
+                        const int64_t *t_ns, const int32_t *free_in, const int64_t *run_cell,
+                        const uint8_t *active, int32_t policy, const int64_t *t_max,
+                        int64_t *decision, int32_t *free_after, double *total_score);
 int oracle_round_state(const oracle_problem *pr, int64_t n_cells, const int32_t *cell_job,
                        const int32_t *cell_type, const int32_t *cell_G, const int32_t *cell_S,
                        const int64_t *t_ns, const int32_t *free_in, const int64_t *run_cell,

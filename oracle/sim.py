@@ -14,7 +14,11 @@ import numpy as np
 NS = 10 ** 9
 
 
-def simulate(o, cells, t_ns, iterations, penalty_s=30):
+def simulate(o, cells, t_ns, iterations, penalty_s=30, policy=0, deadlines=None):
+    """policy: the round's NEXT-4 ablation flags (bit 0 NA, bit 1 NH; R-11).
+    deadlines: absolute ns per job or None (deadline-aware variant, R-12): a
+    pending job no Cell can finish by its deadline is dropped before the round;
+    an option's T must satisfy start + penalty + remaining * T <= deadline."""
     pr = o.pr
     J = pr.n_jobs
     submit = [int(x) * NS for x in pr.submit]
@@ -28,6 +32,11 @@ def simulate(o, cells, t_ns, iterations, penalty_s=30):
     first = [-1] * J
     restarts = [0] * J
     rounds = 0
+    best_T = [None] * J  # fastest feasible Cell of each job
+    for c in range(len(t_ns)):
+        j, T = int(cells["job"][c]), int(t_ns[c])
+        if T != np.iinfo(np.int64).max and (best_T[j] is None or T < best_T[j]):
+            best_T[j] = T
     while True:
         t_next = [fin[j] for j in range(J) if status[j] == "running"]
         t_next += [submit[j] for j in range(J) if status[j] == "future"]
@@ -41,13 +50,31 @@ def simulate(o, cells, t_ns, iterations, penalty_s=30):
         for j in range(J):
             if status[j] == "future" and submit[j] <= t:
                 status[j] = "pending"
+        t_max = None
+        if deadlines is not None:
+            t_max = [-1] * J
+            for j in range(J):
+                if status[j] not in ("pending", "running"):
+                    continue
+                pen_j, rem = 0, left[j]
+                if status[j] == "running":
+                    s0, p0 = seg[j]
+                    ran = t - s0 - p0
+                    done_it = ran // int(t_ns[run[j]]) if ran > 0 else 0
+                    rem = left[j] - min(done_it, left[j])
+                    pen_j = P
+                slack = int(deadlines[j]) - t - pen_j
+                t_max[j] = slack // rem if rem > 0 and slack > 0 else -1
+                if status[j] == "pending" and (best_T[j] is None or best_T[j] > t_max[j]):
+                    status[j] = "dropped"  # no Cell finishes before the deadline
         active = np.array([s in ("pending", "running") for s in status], np.uint8)
         free = [int(c) for c in pr.cap]
         for j in range(J):
             if status[j] == "running":
                 free[int(cells["type"][run[j]])] -= int(cells["G"][run[j]])
         dec, _, _ = o.round_state(cells, t_ns, free, run_cell=np.array(run, np.int64),
-                                  active=active)
+                                  active=active, policy=policy,
+                                  t_max=None if t_max is None else np.array(t_max, np.int64))
         rounds += 1
         for j in range(J):
             if not active[j]:

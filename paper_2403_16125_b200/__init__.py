@@ -77,7 +77,7 @@ EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_update_profile
            "crius_compact_gathered", "crius_exchange_init", "crius_exchange_open",
            "crius_estimate_exchange", "crius_exchange_wait", "crius_exchange_close",
            "crius_schedule_round", "crius_schedule_round_state",
-           "crius_round_stats",
+           "crius_round_stats", "crius_set_round_policy", "crius_set_deadline_bounds",
            "crius_kernel_launches",
            "crius_last_error", "crius_destroy"]
 
@@ -118,6 +118,8 @@ def lib():
         L.crius_schedule_round.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.crius_schedule_round_state.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.crius_round_stats.argtypes = [vp, vp, vp]
+        L.crius_set_round_policy.argtypes = [vp, i32]
+        L.crius_set_deadline_bounds.argtypes = [vp, vp, vp]
         L.crius_kernel_launches.argtypes = [vp]
         L.crius_kernel_launches.restype = i64
         L.crius_last_error.restype = C.c_char_p
@@ -377,6 +379,24 @@ class Crius:
             None if ac is None else _ptr(ac), _ptr(dec), _ptr(fa), C.byref(tot),
             _stream_handle(stream)))
         return dec, fa, tot.value
+
+    def set_round_policy(self, policy):
+        """NEXT-4 ablations: 0 full round, 1 NA (no GPU-count change), 2 NH (no
+        GPU-type change of admitted jobs), 3 both."""
+        _check(lib().crius_set_round_policy(self.ctx, int(policy)))
+
+    def set_deadline_bounds(self, t_max, stream=None):
+        """Per-job bound on an option's iteration time (ns) for later rounds
+        (deadline-aware scheduling, R-12); None removes it."""
+        if t_max is None:
+            _check(lib().crius_set_deadline_bounds(self.ctx, None, _stream_handle(stream)))
+            return
+        a = np.ascontiguousarray(t_max, np.int64)
+        if a.shape != (self.pr.n_jobs,):
+            raise ValueError("t_max must have one entry per job")
+        _check(lib().crius_set_deadline_bounds(self.ctx, _ptr(a), _stream_handle(stream)))
+        # the upload is asynchronous: keep the host array alive until it has run
+        self.torch.cuda.synchronize(self.device)
 
     def round_stats(self, stream=None):
         out = np.zeros(21, np.int64)

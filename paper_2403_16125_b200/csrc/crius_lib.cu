@@ -103,6 +103,9 @@ struct crius_ctx {
   int32_t *d_list = nullptr;
   AdmView adm_glob{};  // admitted-job records in global memory (only when they exceed shared)
   EView eg{};          // (ii) move caches in global memory (rounds listing > kECap jobs)
+  int32_t round_policy = 0;  // crius_set_round_policy (NEXT-4 ablations)
+  int64_t *d_tmax = nullptr;  // crius_set_deadline_bounds: [J] or unset
+  bool has_tmax = false;
   // fused exchange (crius_exchange_*): own window = [flags int64[kMaxRanks] | pad to
   // kXchHdr][2][x_cap] records; x_peer[r] = rank r's window mapped over CUDA IPC
   int32_t x_rank = -1, x_world = 0;
@@ -119,7 +122,7 @@ void free_all(crius_ctx *c) {
   void *ptrs[] = {c->d_ng, c->d_gb, c->d_kst, c->d_L, c->d_off, c->d_submit, c->d_id, c->d_c,
                   c->d_tpn, c->d_w, c->d_act, c->d_bnd, c->d_tpv, c->d_rank, c->d_pi,
                   c->d_pkeys, c->d_pvals, c->d_sort_tmp,
-                  c->d_scratch, c->C.job, c->C.type, c->C.G, c->C.S, c->C.nplans, c->C.plan_off,
+                  c->d_scratch, c->d_tmax, c->C.job, c->C.type, c->C.G, c->C.S, c->C.nplans, c->C.plan_off,
                   c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight,
                   c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
@@ -945,6 +948,8 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   R.T = T;
   R.maxopt = c->maxopt;
   R.depth = c->P.depth;
+  R.policy = c->round_policy;
+  R.tmax = c->has_tmax ? c->d_tmax : nullptr;
   R.rank = c->d_rank;
   R.pi = c->d_pi;
   R.opt = c->d_opt;
@@ -1021,6 +1026,27 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   CK(cudaMemcpyAsync(free_after, c->d_free, T * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(total_score, c->d_total, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return CRIUS_OK;
+}
+
+crius_status crius_set_round_policy(crius_ctx *c, int32_t policy) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  if (policy < 0 || policy > 3) return fail(CRIUS_EINVAL, "round policy must be 0..3 (bit 0 NA, bit 1 NH)");
+  c->round_policy = policy;
+  return CRIUS_OK;
+}
+
+crius_status crius_set_deadline_bounds(crius_ctx *c, const int64_t *t_max, void *stream) {
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  if (!t_max) {
+    c->has_tmax = false;
+    return CRIUS_OK;
+  }
+  CK(cudaSetDevice(c->device));
+  if (!c->d_tmax) CK(dalloc(&c->d_tmax, c->P.J));
+  CK(cudaMemcpyAsync(c->d_tmax, t_max, (size_t)c->P.J * 8, cudaMemcpyHostToDevice,
+                     (cudaStream_t)stream));
+  c->has_tmax = true;
   return CRIUS_OK;
 }
 

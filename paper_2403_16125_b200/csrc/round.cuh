@@ -50,6 +50,9 @@ struct EView {
 
 struct RoundBuf {
   int32_t J, T, maxopt, depth;
+  int32_t policy;        // NEXT-4 ablations (R-11): bit 0 NA (options at G = N_G only),
+                         // bit 1 NH (admitted jobs keep their GPU type)
+  const int64_t *tmax;   // [J] by job or NULL: deadline bound on an option's T (R-12)
   const int32_t *rank;   // [J] job -> priority position
   const int32_t *pi;     // [J] position -> job
   OptRec *opt;           // [J][maxopt] by position, (t, G) ascending
@@ -91,12 +94,19 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
   int n = 0;
   int64_t ref_ng = kInf, ref_any = kInf;
   int lastT = -1, lastG = -1;
+  const bool act0 = R.active ? R.active[j] != 0 : true;
+  const int64_t rc0 = (act0 && R.run_cell) ? R.run_cell[j] : -1;
+  const int64_t tmx = R.tmax ? R.tmax[j] : kInf;
   for (int64_t c = c0; c < c1; ++c) {
     const int64_t T = res[c].t_ns;
     const int t = cType[c], G = cG[c];
     if (T == kInf) continue;
     ref_any = min(ref_any, T);
     if (G == ngj) ref_ng = min(ref_ng, T);
+    if ((R.policy & 1) && G != ngj) continue;  // NA: the job stays at N_G GPUs
+    // deadline: a Cell slower than the job's bound is no option, except the
+    // (type, G) the job runs on (its completion was guaranteed at placement)
+    if (T > tmx && !(rc0 >= 0 && t == cType[rc0] && G == cG[rc0])) continue;
     if (t == lastT && G == lastG) {
       if (T < o[n - 1].T) {  // equal T keeps the earlier (smaller S) Cell
         o[n - 1].T = T;
@@ -587,7 +597,7 @@ __device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmVi
       int fm = -1;
       for (int q = 0; q < TT; ++q)
         if (q != tid) fm = max(fm, sh.fr[q]);
-      sh.fmax_other[tid] = fm;
+      sh.fmax_other[tid] = (R.policy & 2) ? -1 : fm;  // NH: no other-type victim move
     }
   }
   if (tid < TT * TT && !sh.seq_ok[tid / TT]) {
@@ -994,7 +1004,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
         opt = warp_best_option(R.opt + (int64_t)pos * R.maxopt, A.nopt[a],
                                [&](int i, const OptRec &x) {
                                  const int avail = sh.fr[x.t] + (x.t == tc ? Gc : 0);
-                                 return i != cv && x.G <= avail && x.T < Tc;
+                                 return i != cv && x.G <= avail && x.T < Tc &&
+                                        (!(R.policy & 2) || x.t == tc);  // NH keeps the type
                                });
       }
       if (lane == 0) {

@@ -50,15 +50,42 @@ class SimResult:
                 "avg_restarts": float(self.restarts[done].mean()) if done.any() else None}
 
 
-def simulate(cr, pr, iterations, penalty_s=30, results=None):
-    """Replay the Problem's trace through GPU rounds; `cr` is a Crius context."""
+def simulate(cr, pr, iterations, penalty_s=30, results=None, policy=0, deadlines=None):
+    """Replay the Problem's trace through GPU rounds; `cr` is a Crius context.
+    policy: the round's ablation flags (bit 0 NA: no GPU-count scaling, bit 1 NH:
+    no GPU-type scaling), set for this run and reset after.
+    deadlines: absolute ns per job, or None -- the deadline-aware variant
+    (reading R-12): before each round a pending job that no
+    Cell can finish in time is dropped, and every job's options are bounded by
+    t_max = floor((D - t - penalty) / remaining) (penalty only for a running
+    job, which would restart), so every placement meets its deadline."""
+    cr.set_round_policy(policy)
+    try:
+        return _simulate(cr, pr, iterations, penalty_s, results, deadlines)
+    finally:
+        cr.set_round_policy(0)
+        cr.set_deadline_bounds(None)
+
+
+def deadline_bound(D, t, pen, rem):
+    """Largest iteration time that finishes `rem` iterations by D after a start
+    (or restart, pen > 0) at t; -1 if none does."""
+    if rem <= 0 or D - t - pen <= 0:
+        return -1
+    return (D - t - pen) // rem
+
+
+def _simulate(cr, pr, iterations, penalty_s, results, deadlines):
     J = pr.n_jobs
     if cr.n_cells is None:
         cr.enumerate()
     if results is None:
         results = cr.estimate()
-    cells = {k: v.cpu().numpy() for k, v in cr.cells().items() if k in ("type", "G")}
+    cells = {k: v.cpu().numpy() for k, v in cr.cells().items() if k in ("job", "type", "G")}
     t_cell = results[:cr.n_cells, 0].cpu().numpy()
+    INF = np.iinfo(np.int64).max
+    t_best = np.full(J, INF, np.int64)  # fastest feasible Cell per job (early drop)
+    np.minimum.at(t_best, cells["job"], t_cell)
     submit = np.asarray(pr.submit, np.int64) * NS
     iters = np.asarray(iterations, np.int64)
     pen = int(penalty_s) * NS
@@ -87,6 +114,19 @@ def simulate(cr, pr, iterations, penalty_s=30, results=None):
         while nxt < J and submit[order[nxt]] <= t:
             state[order[nxt]] = PENDING
             nxt += 1
+        if deadlines is not None:
+            tmax = np.full(J, -1, np.int64)
+            for j in np.where((state == PENDING) | (state == RUNNING))[0]:
+                if state[j] == RUNNING:
+                    ran = t - seg_start[j] - seg_pen[j]
+                    done_it = ran // int(t_cell[run[j]]) if ran > 0 else 0
+                    tmax[j] = deadline_bound(int(deadlines[j]), int(t), pen,
+                                             int(remaining[j]) - min(done_it, int(remaining[j])))
+                else:
+                    tmax[j] = deadline_bound(int(deadlines[j]), int(t), 0, int(remaining[j]))
+                    if t_best[j] > tmax[j]:
+                        state[j] = DROPPED  # early drop: no Cell finishes in time
+            cr.set_deadline_bounds(tmax)
         active = ((state == PENDING) | (state == RUNNING)).astype(np.uint8)
         used = np.zeros(pr.n_types, np.int64)
         for j in np.where(state == RUNNING)[0]:

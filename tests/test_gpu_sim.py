@@ -39,3 +39,47 @@ def test_sim_matches_oracle(pkg, oracle_mod, cfg, n, depth, pen):
     assert np.array_equal(got.finish, want["finish"])
     assert np.array_equal(got.restarts, want["restarts"])
     assert np.array_equal(got.state, want["state"])
+
+
+@pytest.mark.parametrize("policy", [1, 2, 3])
+def test_sim_policy_matches_oracle(pkg, oracle_mod, policy):
+    """The ablation runs (NA / NH / both) of the simulator match the oracle's."""
+    from oracle import sim as osim
+    from paper_2403_16125_b200 import sim
+    pr = W.subset(W.make_config(3), 150)
+    it = W.iterations_for(pr, seed=3)
+    with pkg.Crius(pr) as cr:
+        got = sim.simulate(cr, pr, it, penalty_s=30, policy=policy)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    t_ns, _ = o.estimate(cells)
+    want = osim.simulate(o, cells, t_ns, it, 30, policy=policy)
+    assert got.rounds == want["rounds"]
+    assert np.array_equal(got.first_start, want["first_start"])
+    assert np.array_equal(got.finish, want["finish"])
+    assert np.array_equal(got.restarts, want["restarts"])
+    assert np.array_equal(got.state, want["state"])
+
+
+@pytest.mark.parametrize("cfg,n,policy", [(2, 8, 0), (3, 150, 0), (3, 150, 2)])
+def test_sim_deadlines_match_oracle(pkg, oracle_mod, cfg, n, policy):
+    """The deadline-aware simulation (early drops + t_max-bounded options)
+    matches the oracle's; finished jobs meet their deadlines."""
+    from oracle import sim as osim
+    from paper_2403_16125_b200 import sim
+    from test_sim_pins import deadlines_for
+    pr = W.subset(W.make_config(cfg), n)
+    pr.depth = 3
+    it = W.iterations_for(pr, seed=cfg)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    t_ns, _ = o.estimate(cells)
+    dl = deadlines_for(pr, cells, t_ns, it, seed=cfg + 40)
+    with pkg.Crius(pr) as cr:
+        got = sim.simulate(cr, pr, it, penalty_s=30, policy=policy, deadlines=dl)
+    want = osim.simulate(o, cells, t_ns, it, 30, policy=policy, deadlines=dl)
+    assert got.rounds == want["rounds"]
+    for k in ("first_start", "finish", "restarts", "state"):
+        assert np.array_equal(getattr(got, k), want[k]), k
+    done = got.state == sim.DONE
+    assert np.all(got.finish[done] <= dl[done])
