@@ -931,14 +931,19 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
   if (lane == 0) un = A.unit_begin + atomicAdd(A.work_counter, 1);
   un = __shfl_sync(0xffffffffu, un, 0);
   UnitMeta nm = load_meta(P, A, un);
+  // work tickets run one unit ahead: the ticket drawn now is consumed by the
+  // next iteration, so the atomic's round trip hides behind a whole unit
+  int ticket = 0;
+  if (lane == 0) ticket = atomicAdd(A.work_counter, 1);
 
   for (;;) {
     const UnitMeta m = nm;
     const int64_t u = m.u;
     if (u >= A.unit_end) break;
-    // grab and prefetch the metadata of the next unit while this one runs
-    if (lane == 0) un = A.unit_begin + atomicAdd(A.work_counter, 1);
-    un = __shfl_sync(0xffffffffu, un, 0);
+    // prefetch the metadata of the next unit (last iteration's ticket) and
+    // draw the ticket after it
+    un = A.unit_begin + __shfl_sync(0xffffffffu, ticket, 0);
+    if (lane == 0) ticket = atomicAdd(A.work_counter, 1);
     nm = load_meta(P, A, un);
 
     const int t = (int)(u % P.T);
@@ -990,11 +995,23 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
     gmax = warp_max_int(gmax);
     const int K1u = ilog2_pow2(gmax) + 1;  // <= K1s
     CRIUS_CHECK(K1u <= K1s && smax <= A.Stop);
-    for (int k = 0; k < K1u; ++k) warp_prefix32(PC + k * Lp, CRAW + k * Lp, L, lane);
+    // int32 rows (K1u compute rows + tp_calls): one lane per row, a serial scan
+    // whose loads do not depend on the running sum (no shuffle rounds)
+    if (lane <= K1u) {
+      const int32_t *src = lane < K1u ? CRAW + lane * Lp : NRAW;
+      int64_t *dst = lane < K1u ? PC + lane * Lp : PN;
+      int64_t acc = 0;
+      dst[0] = 0;
+#pragma unroll 8
+      for (int l = 0; l < L; ++l) {
+        acc += src[l];
+        dst[l + 1] = acc;
+      }
+    }
+    __syncwarp();
     warp_prefix_inplace(PW, L, lane);
     warp_prefix_inplace(PA, L, lane);
     warp_prefix_inplace(PV, L, lane);
-    warp_prefix32(PN, NRAW, L, lane);
     __syncwarp();
 
     const int nSi = ilog2_pow2(smax) + 1;
