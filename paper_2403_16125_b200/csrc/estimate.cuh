@@ -995,8 +995,10 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
     gmax = warp_max_int(gmax);
     const int K1u = ilog2_pow2(gmax) + 1;  // <= K1s
     CRIUS_CHECK(K1u <= K1s && smax <= A.Stop);
-    // int32 rows (K1u compute rows + tp_calls): one lane per row, a serial scan
-    // whose loads do not depend on the running sum (no shuffle rounds)
+    // every row by one lane, a serial scan whose loads do not depend on the
+    // running sum (no shuffle rounds): lanes 0..K1u the int32 rows (K1u compute
+    // rows + tp_calls) into their int64 prefix rows, lanes 29..31 the int64
+    // rows w, act, tpv in place
     if (lane <= K1u) {
       const int32_t *src = lane < K1u ? CRAW + lane * Lp : NRAW;
       int64_t *dst = lane < K1u ? PC + lane * Lp : PN;
@@ -1007,11 +1009,16 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
         acc += src[l];
         dst[l + 1] = acc;
       }
+    } else if (lane >= 29) {
+      int64_t *x = lane == 29 ? PW : (lane == 30 ? PA : PV);
+      int64_t acc = 0;
+      x[0] = 0;
+#pragma unroll 8
+      for (int l = 1; l <= L; ++l) {
+        acc += x[l];
+        x[l] = acc;
+      }
     }
-    __syncwarp();
-    warp_prefix_inplace(PW, L, lane);
-    warp_prefix_inplace(PA, L, lane);
-    warp_prefix_inplace(PV, L, lane);
     __syncwarp();
 
     const int nSi = ilog2_pow2(smax) + 1;
