@@ -111,8 +111,16 @@ __device__ __forceinline__ int64_t warp_incl_scan(int64_t x, int lane) {
 }
 
 __device__ __forceinline__ int warp_max_int(int x) {
+  return __reduce_max_sync(0xffffffffu, x);  // redux.sync: one instruction, no shuffle rounds
+}
+
+// Warp-wide inclusive scan of int32 values (one shuffle per step).
+__device__ __forceinline__ int warp_incl_scan32(int x, int lane) {
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, d));
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
   return x;
 }
 

@@ -1184,7 +1184,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
     }
     __syncwarp();
     {
-      int64_t carry = 0;
+      int carry = 0;  // item counts: <= maxCells * (k_max + 1) * groups, int32
       for (int b0 = 0; b0 < nc; b0 += 32) {
         const int r = b0 + lane;
         int cnt = 0;
@@ -1192,8 +1192,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
           const int ci = ORD[r];
           cnt = (ilog2_pow2(CG[ci] / CS[ci]) + 1) * ngrp;
         }
-        const int64_t inc = warp_incl_scan((int64_t)cnt, lane);
-        if (r < nc) CP[r + 1] = (int)(carry + inc);
+        const int inc = warp_incl_scan32(cnt, lane);
+        if (r < nc) CP[r + 1] = carry + inc;
         carry += __shfl_sync(0xffffffffu, inc, 31);
       }
       if (lane == 0) CP[0] = 0;
