@@ -86,20 +86,6 @@ __device__ __forceinline__ void exchange_signal(const EstArgs &A) {
 // A rank with an empty unit range still signals its (empty) contribution.
 __global__ void k_xch_signal_only(EstArgs A) { exchange_signal(A); }
 
-// Inclusive prefix of a profile row into dst[0..L] (dst[0] = 0).
-template <typename Src>
-__device__ __forceinline__ void warp_prefix(int64_t *dst, const Src *__restrict__ src, int L,
-                                            int lane) {
-  int64_t carry = 0;
-  if (lane == 0) dst[0] = 0;
-  for (int b = 0; b < L; b += 32) {
-    const int64_t x = (b + lane < L) ? (int64_t)__ldg(src + b + lane) : 0;
-    const int64_t inc = warp_incl_scan(x, lane);
-    if (b + lane < L) dst[b + lane + 1] = carry + inc;
-    carry += __shfl_sync(0xffffffffu, inc, 31);
-  }
-}
-
 struct UnitCtx {
   const int64_t *PC, *PW, *PA, *PV, *PN, *BND;
   const int16_t *BD;
@@ -775,31 +761,6 @@ __device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
-
-// In-place inclusive prefix of x[1..L] (x[0] := 0); int64 entries in shared memory.
-__device__ __forceinline__ void warp_prefix_inplace(int64_t *x, int L, int lane) {
-  int64_t carry = 0;
-  for (int b = 0; b < L; b += 32) {
-    const int64_t v = (b + lane < L) ? x[b + lane + 1] : 0;
-    const int64_t inc = warp_incl_scan(v, lane);
-    __syncwarp();
-    if (b + lane < L) x[b + lane + 1] = carry + inc;
-    carry += __shfl_sync(0xffffffffu, inc, 31);
-  }
-  if (lane == 0) x[0] = 0;
-}
-
-// Inclusive prefix of an int32 shared-memory row src[0..L) into dst[0..L].
-__device__ __forceinline__ void warp_prefix32(int64_t *dst, const int32_t *src, int L, int lane) {
-  int64_t carry = 0;
-  if (lane == 0) dst[0] = 0;
-  for (int b = 0; b < L; b += 32) {
-    const int64_t v = (b + lane < L) ? (int64_t)src[b + lane] : 0;
-    const int64_t inc = warp_incl_scan(v, lane);
-    if (b + lane < L) dst[b + lane + 1] = carry + inc;
-    carry += __shfl_sync(0xffffffffu, inc, 31);
-  }
 }
 
 // K2 rows f[2..smax] (lowest-argmin binary search, §N3), in the narrowest
