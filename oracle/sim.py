@@ -2,7 +2,7 @@
 
 A plain, literal event loop over the oracle's round (oracle_round_state),
 written independently of paper_2403_16125_b200/sim.py; the two share no code.
-Semantics (reading R-8), integer nanoseconds:
+Semantics (reading R-13), integer nanoseconds:
   - first start on Cell c at time s: finish = s + N * T(c)      (N iterations)
   - restart (Cell change) at time t: the segment's completed iterations
     floor((t - s - pen_seg) / T(c_old)) are kept; finish = t + P + N' * T(c_new)

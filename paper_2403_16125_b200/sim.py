@@ -7,7 +7,7 @@ scheduling decision here is one `crius_schedule_round_state` call on the GPU
 (running jobs keep their Cells unless downscaled/moved as victims or scaled up
 in Phase B); this module only keeps the event clock and job states.
 
-Event semantics (reading R-8), all integer nanoseconds:
+Event semantics (reading R-13), all integer nanoseconds:
   * a job with N iterations started on Cell c at time s finishes at
     s + penalty + N * T(c) (T = the Cell's estimated iteration time); the
     penalty is paid on every restart (Cell change), not on the first start;
