@@ -50,7 +50,8 @@ class SimResult:
                 "avg_restarts": float(self.restarts[done].mean()) if done.any() else None}
 
 
-def simulate(cr, pr, iterations, penalty_s=30, results=None, policy=0, deadlines=None):
+def simulate(cr, pr, iterations, penalty_s=30, results=None, policy=0, deadlines=None,
+             opportunistic=False):
     """Replay the Problem's trace through GPU rounds; `cr` is a Crius context.
     policy: the round's ablation flags (bit 0 NA: no GPU-count scaling, bit 1 NH:
     no GPU-type scaling), set for this run and reset after.
@@ -58,10 +59,18 @@ def simulate(cr, pr, iterations, penalty_s=30, results=None, policy=0, deadlines
     (reading R-12): before each round a pending job that no
     Cell can finish in time is dropped, and every job's options are bounded by
     t_max = floor((D - t - penalty) / remaining) (penalty only for a running
-    job, which would restart), so every placement meets its deadline."""
+    job, which would restart), so every placement meets its deadline.
+    opportunistic: opportunistic execution (reading R-14): a
+    running job is opportunistic while a job of earlier priority is pending;
+    before a round, a pending job that fits nowhere directly but would fit on a
+    type once the opportunistic jobs of later priority there are suspended gets
+    them suspended (latest priority first, until its smallest option on that
+    type fits; the type with the smallest such option, lowest index on ties).
+    A suspended job keeps its completed iterations and pays the restart
+    penalty when it resumes."""
     cr.set_round_policy(policy)
     try:
-        return _simulate(cr, pr, iterations, penalty_s, results, deadlines)
+        return _simulate(cr, pr, iterations, penalty_s, results, deadlines, opportunistic)
     finally:
         cr.set_round_policy(0)
         cr.set_deadline_bounds(None)
@@ -75,7 +84,39 @@ def deadline_bound(D, t, pen, rem):
     return (D - t - pen) // rem
 
 
-def _simulate(cr, pr, iterations, penalty_s, results, deadlines):
+def _suspend_for_pending(state, run, rank, opp, gmin_t, free, cells, suspend):
+    """Opportunistic execution (R-14): suspend later-priority opportunistic jobs
+    for each pending job, in priority order; returns the suspended jobs."""
+    BIG = np.iinfo(np.int64).max
+    out = []
+    for p in np.argsort(rank):
+        if state[p] != PENDING:
+            continue
+        g_row = gmin_t[p]
+        if np.any((g_row < BIG) & (g_row <= free)):
+            continue  # fits directly: the round places it
+        best = None
+        for tt in range(len(free)):
+            if g_row[tt] >= BIG:
+                continue
+            cand = [j for j in np.where((state == RUNNING) & opp)[0]
+                    if cells["type"][run[j]] == tt and rank[j] > rank[p]]
+            room = int(free[tt]) + sum(int(cells["G"][run[j]]) for j in cand)
+            if room >= g_row[tt] and (best is None or (int(g_row[tt]), tt) < best[:2]):
+                best = (int(g_row[tt]), tt, cand)
+        if best is None:
+            continue
+        g, tt, cand = best
+        for v in sorted(cand, key=lambda j: -rank[j]):
+            if free[tt] >= g:
+                break
+            free[tt] += int(cells["G"][run[v]])
+            suspend(v)
+            out.append(v)
+    return out
+
+
+def _simulate(cr, pr, iterations, penalty_s, results, deadlines, opportunistic):
     J = pr.n_jobs
     if cr.n_cells is None:
         cr.enumerate()
@@ -98,6 +139,21 @@ def _simulate(cr, pr, iterations, penalty_s, results, deadlines):
     first = np.full(J, -1, np.int64)
     restarts = np.zeros(J, np.int32)
     events = []
+    # priority (submit, id) and, per job and type, its smallest option G (<= N_G)
+    rank = np.empty(J, np.int64)
+    rank[np.lexsort((np.asarray(pr.job_id), np.asarray(pr.submit)))] = np.arange(J)
+    opp = np.zeros(J, bool)
+    resumed = np.zeros(J, bool)
+    gmin_t = np.full((J, pr.n_types), INF, np.int64)
+    okc = (t_cell != INF) & (cells["G"] <= np.asarray(pr.ng)[cells["job"]])
+    np.minimum.at(gmin_t, (cells["job"][okc], cells["type"][okc]), cells["G"][okc])
+
+    def suspend(v):
+        ran = t - seg_start[v] - seg_pen[v]
+        done_it = ran // int(t_cell[run[v]]) if ran > 0 else 0
+        remaining[v] -= min(done_it, remaining[v])
+        state[v], run[v], opp[v], resumed[v] = PENDING, -1, False, True
+
     order = np.argsort(submit, kind="stable")
     nxt = 0
     t = 0
@@ -114,6 +170,12 @@ def _simulate(cr, pr, iterations, penalty_s, results, deadlines):
         while nxt < J and submit[order[nxt]] <= t:
             state[order[nxt]] = PENDING
             nxt += 1
+        if opportunistic:
+            used = np.zeros(pr.n_types, np.int64)
+            for j in np.where(state == RUNNING)[0]:
+                used[cells["type"][run[j]]] += cells["G"][run[j]]
+            _suspend_for_pending(state, run, rank, opp, gmin_t,
+                                 np.asarray(pr.cap, np.int64) - used, cells, suspend)
         if deadlines is not None:
             tmax = np.full(J, -1, np.int64)
             for j in np.where((state == PENDING) | (state == RUNNING))[0]:
@@ -123,7 +185,8 @@ def _simulate(cr, pr, iterations, penalty_s, results, deadlines):
                     tmax[j] = deadline_bound(int(deadlines[j]), int(t), pen,
                                              int(remaining[j]) - min(done_it, int(remaining[j])))
                 else:
-                    tmax[j] = deadline_bound(int(deadlines[j]), int(t), 0, int(remaining[j]))
+                    tmax[j] = deadline_bound(int(deadlines[j]), int(t), pen if resumed[j] else 0,
+                                             int(remaining[j]))
                     if t_best[j] > tmax[j]:
                         state[j] = DROPPED  # early drop: no Cell finishes in time
             cr.set_deadline_bounds(tmax)
@@ -140,11 +203,15 @@ def _simulate(cr, pr, iterations, penalty_s, results, deadlines):
                 state[j] = DROPPED
             elif d >= 0:
                 if state[j] == PENDING:
+                    p0 = pen if resumed[j] else 0  # a suspended job resumes with a restart
                     state[j] = RUNNING
-                    run[j], seg_start[j], seg_pen[j] = d, t, 0
+                    run[j], seg_start[j], seg_pen[j] = d, t, p0
                     if first[j] < 0:
                         first[j] = t
-                    finish[j] = t + int(remaining[j]) * int(t_cell[d])
+                    finish[j] = t + p0 + int(remaining[j]) * int(t_cell[d])
+                    if resumed[j]:
+                        restarts[j] += 1
+                        resumed[j] = False
                     n_start += 1
                 elif d != run[j]:
                     ran = t - seg_start[j] - seg_pen[j]
@@ -154,6 +221,10 @@ def _simulate(cr, pr, iterations, penalty_s, results, deadlines):
                     finish[j] = t + pen + int(remaining[j]) * int(t_cell[d])
                     restarts[j] += 1
                     n_restart += 1
+        if opportunistic:  # opportunistic = running while an earlier job waits
+            pend = np.where(state == PENDING)[0]
+            first_wait = rank[pend].min() if pend.size else J
+            opp[:] = (state == RUNNING) & (rank > first_wait)
         events.append((int(t), n_start, n_restart, int(ended.size)))
     state[state == PENDING] = STARVED
     return SimResult(first, finish, restarts, state, len(events), events)

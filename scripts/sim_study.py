@@ -20,6 +20,8 @@ ap.add_argument("--jobs", type=int, default=0)
 ap.add_argument("--depths", default="0,1,3")
 ap.add_argument("--penalty", type=int, default=30)
 ap.add_argument("--policies", default="0", help="0 full, 1 NA, 2 NH, 3 both")
+ap.add_argument("--opportunistic", action="store_true",
+                help="opportunistic execution (suspend later jobs for a waiting one, PAPER.md:504-507)")
 ap.add_argument("--deadlines", type=float, default=0.0,
                 help="> 0: deadline-aware runs, deadline = submit + U[lo, hi] x N x fastest T, "
                      "lo = this value, hi = 2.5 (ElasticFlow-style, PAPER.md:753-780)")
@@ -44,7 +46,8 @@ for pol in [int(x) for x in a.policies.split(",")]:
                 lam = np.random.default_rng(a.config).uniform(a.deadlines, 2.5, base.n_jobs)
                 dl = base.submit.astype(np.int64) * sim.NS + (lam * best * it).astype(np.int64)
             t0 = time.perf_counter()
-            r = sim.simulate(cr, base, it, penalty_s=a.penalty, policy=pol, deadlines=dl)
+            r = sim.simulate(cr, base, it, penalty_s=a.penalty, policy=pol, deadlines=dl,
+                             opportunistic=a.opportunistic)
             dt = time.perf_counter() - t0
         s = r.summary(base.submit.astype(np.int64) * sim.NS)
         done = r.state == sim.DONE
@@ -54,6 +57,6 @@ for pol in [int(x) for x in a.policies.split(",")]:
         if dl is not None:
             s["deadline_ratio"] = float((done & (r.finish <= dl)).sum() / base.n_jobs)
         s.update(config=base.name, depth=d, policy=["full", "NA", "NH", "NA+NH"][pol],
-                 deadlines=a.deadlines or None,
+                 deadlines=a.deadlines or None, opportunistic=a.opportunistic,
                  wall_s=round(dt, 2), rounds_per_s=round(r.rounds / dt, 1))
         print(json.dumps(s), flush=True)

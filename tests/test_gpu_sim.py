@@ -83,3 +83,26 @@ def test_sim_deadlines_match_oracle(pkg, oracle_mod, cfg, n, policy):
         assert np.array_equal(getattr(got, k), want[k]), k
     done = got.state == sim.DONE
     assert np.all(got.finish[done] <= dl[done])
+
+
+@pytest.mark.parametrize("cfg,n,depth,policy,ddl", [(2, 8, 0, 0, False), (3, 150, 3, 0, False),
+                                                   (3, 150, 0, 0, False), (3, 150, 3, 2, True)])
+def test_sim_opportunistic_matches_oracle(pkg, oracle_mod, cfg, n, depth, policy, ddl):
+    """Opportunistic execution (R-14; with NH and deadlines in the last case):
+    suspensions, resumptions and every event time identical to the oracle's."""
+    from oracle import sim as osim
+    from paper_2403_16125_b200 import sim
+    from test_sim_pins import deadlines_for
+    pr = W.subset(W.make_config(cfg), n)
+    pr.depth = depth
+    it = W.iterations_for(pr, seed=cfg)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    t_ns, _ = o.estimate(cells)
+    dl = deadlines_for(pr, cells, t_ns, it, seed=cfg + 50) if ddl else None
+    with pkg.Crius(pr) as cr:
+        got = sim.simulate(cr, pr, it, penalty_s=30, policy=policy, deadlines=dl, opportunistic=True)
+    want = osim.simulate(o, cells, t_ns, it, 30, policy=policy, deadlines=dl, opportunistic=True)
+    assert got.rounds == want["rounds"]
+    for k in ("first_start", "finish", "restarts", "state"):
+        assert np.array_equal(getattr(got, k), want[k]), k

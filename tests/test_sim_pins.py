@@ -160,3 +160,37 @@ def deadlines_for(pr, cells, t_ns, it, seed):
     lam = rng.uniform(0.8, 2.5, pr.n_jobs)
     base = np.where(best == INF, 0, best).astype(np.float64) * np.asarray(it, np.float64)
     return (np.asarray(pr.submit, np.int64) * NS + (lam * base).astype(np.int64)).astype(np.int64)
+
+
+# ---------------------------------------------------------------- opportunistic execution (R-14)
+def test_opportunistic_hand_trace(oracle_mod):
+    """PAPER.md:504-507 on a hand trace (tests/golden/sim_opportunistic.json)."""
+    from oracle import sim
+    fx = golden("sim_opportunistic.json")
+    pr, cells, t_ns = _round_problem(fx, 0)
+    it = [j["iters"] for j in fx["jobs"]]
+    for key, opp in (("plain", False), ("opportunistic", True)):
+        out = sim.simulate(oracle_mod.Oracle(pr), cells, t_ns, it, fx["penalty_s"], opportunistic=opp)
+        e = fx["expect"][key]
+        assert list(out["first_start"] // NS) == e["first_start_s"], key
+        assert list(out["finish"] // NS) == e["finish_s"], key
+        assert list(out["restarts"]) == e["restarts"], key
+        assert np.all(out["state"] == 3), key
+
+
+def test_opportunistic_invariants(oracle_mod):
+    """With opportunistic execution every job still finishes at most once and
+    never faster than its iterations on its fastest Cell; suspended jobs are
+    counted as restarts."""
+    from oracle import sim
+    pr = W.subset(W.make_config(3), 120)
+    o = oracle_mod.Oracle(pr)
+    cells = o.enumerate()
+    t_ns, _ = o.estimate(cells)
+    it = W.iterations_for(pr)
+    out = sim.simulate(o, cells, t_ns, it, 30, opportunistic=True)
+    done = out["state"] == 3
+    assert done.sum() + (out["state"] == 4).sum() + (out["state"] == 5).sum() == pr.n_jobs
+    for j in np.where(done)[0]:
+        best = t_ns[(cells["job"] == j) & (t_ns < np.iinfo(np.int64).max)].min()
+        assert out["finish"][j] - out["first_start"][j] >= it[j] * best
