@@ -20,6 +20,13 @@ def _port():
     return p
 
 
+def _make(cfg):
+    from paper_2403_16125_b200 import workload as W
+    if isinstance(cfg, str):  # "tiny<seed>": one job, one GPU type -> one unit
+        return W.random_tiny(int(cfg[4:]), n_types=1, n_jobs=1)
+    return W.make_config(cfg)
+
+
 def _worker_p2p(rank, world, port, cfg, steps, q):
     """The fused exchange: estimate kernel -> P2P stores into every rank's window
     + arrival flags; several steps (double-buffered windows, epochs)."""
@@ -31,7 +38,7 @@ def _worker_p2p(rank, world, port, cfg, steps, q):
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", rank))
-    pr = W.make_config(cfg)
+    pr = _make(cfg)
     outs = []
     with pkg.Crius(pr, device=rank) as cr:
         cr.enumerate()
@@ -93,8 +100,10 @@ def test_nccl_sharded_equals_oracle(oracle_mod, cfg):
         assert np.array_equal(dec, d_ref) and np.array_equal(fa, f_ref) and tot == tot_ref, rank
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("cfg", [3, 4, "tiny7"])
 def test_p2p_exchange_equals_oracle(oracle_mod, cfg):
+    """("tiny7": a single unit, so every rank but one has an empty range and
+    only signals.)"""
     """Fused estimate + NVLink P2P exchange on every GPU of the box (<= 8): every
     rank's records and decisions byte-identical to the oracle, 3 steps each."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
@@ -112,7 +121,7 @@ def test_p2p_exchange_equals_oracle(oracle_mod, cfg):
     for p in ps:
         p.join(timeout=120)
         assert p.exitcode == 0
-    o = oracle_mod.Oracle(W.make_config(cfg))
+    o = oracle_mod.Oracle(_make(cfg))
     cells = o.enumerate()
     t_ref, p_ref = o.estimate(cells)
     d_ref, f_ref, tot_ref = o.round(cells, t_ref)
