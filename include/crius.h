@@ -52,7 +52,7 @@ typedef enum {
 /* GPU types (Table sim_cluster).  Host pointers, read during the
  * call only.  capacity and gpus_per_node are powers of two (A-19, A-20). */
 typedef struct {
-  int32_t n_types;                 /* 1..16 */
+  int32_t n_types;                 /* 1..8 (the round's shared-memory tables) */
   const int32_t *capacity;         /* [n_types] GPUs of this type in the cluster */
   const int32_t *gpus_per_node;    /* [n_types] node size: link class boundary (A-15) */
   const int64_t *mem_bytes;        /* [n_types] per-GPU memory (memory filter) */
@@ -65,7 +65,8 @@ typedef struct {
 /* Jobs and their profiles (decoupled computation/communication).
  * Host pointers, read during the call only. */
 typedef struct {
-  int32_t n_jobs;                  /* >= 1 */
+  int32_t n_jobs;                  /* 1 .. 2^24 - 1 (the round's tie keys hold a
+                                      priority position in 24 bits) */
   int32_t k_max;                   /* compute profiled for tp = 2^0 .. 2^k_max, k_max <= 6 */
   const int64_t *job_id;           /* [n_jobs] unique; priority = (submit, id) ascending (A-18) */
   const int64_t *submit_time;      /* [n_jobs] */
@@ -330,16 +331,15 @@ crius_status crius_set_round_policy(crius_ctx *ctx, int32_t policy);
  * upload on `stream`. */
 crius_status crius_set_deadline_bounds(crius_ctx *ctx, const int64_t *t_max, void *stream);
 
-/* Counters of the last round (HOST out16[21]): [0] speculative Phase A batches,
- * [1] victim-sequence recomputations, [2] SM cycles in them, [3] SM cycles of
- * Phase A, [4] SM cycles of Phase B, [5] admitted jobs, [6] admissions through
- * ScaleResource, [7] Phase B batches, [8..13] cycle/size breakdown of the
- * sequence recomputations (setup + stale same-type caches, listing, other-type
- * caches, the per-type move loops, stale caches refreshed, jobs listed for
- * other-type moves), [14] per-type sequence
- * invalidations, [15..18] cycles of the Phase A
- * batches (window staging, evaluation, ScaleResource incl. sequences, commit).
- * Synchronises `stream`. */
+/* Counters of the last round (HOST int64 out[24]): [0] speculative Phase A
+ * batches, [1] victim-sequence recomputations, [2] SM cycles in them, [3] SM
+ * cycles of Phase A, [4] SM cycles of Phase B, [5] admitted jobs, [6]
+ * admissions through ScaleResource, [7] Phase B batches, [8..10] SM cycles of
+ * the Phase A batches (direct evaluation; sequences + ScaleResource
+ * evaluation; commit), [11] stale same-type move caches refreshed, [12]
+ * other-type move evaluations, [13] per-type sequence invalidations, [14] 1 if
+ * the admitted records lived in shared memory, [15] the round's bound on the
+ * number of admitted records.  Synchronises `stream`. */
 crius_status crius_round_stats(crius_ctx *ctx, int64_t *out16, void *stream);
 
 /* Number of kernels this context has launched so far (for launch accounting). */

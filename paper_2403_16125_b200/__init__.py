@@ -399,13 +399,14 @@ class Crius:
         self.torch.cuda.synchronize(self.device)
 
     def round_stats(self, stream=None):
-        out = np.zeros(21, np.int64)
+        out = np.zeros(32, np.int64)
         _check(lib().crius_round_stats(self.ctx, _ptr(out), _stream_handle(stream)))
         keys = ("phaseA_batches", "seq_recomputes", "seq_cycles", "phaseA_cycles", "phaseB_cycles",
-                "admitted", "scale_admits", "phaseB_batches", "seq_setup_cycles",
-                "seq_listing_cycles", "seq_other_type_cycles", "seq_sequence_cycles",
-                "stale_caches", "other_type_scans", "seq_invalidations", "batch_window_cycles",
-                "batch_eval_cycles", "batch_scale_cycles", "batch_commit_cycles")
+                "admitted", "scale_admits", "phaseB_batches", "batch_direct_cycles",
+                "batch_scale_cycles", "batch_commit_cycles", "stale_caches", "other_type_evals",
+                "seq_invalidations", "records_in_smem", "records_bound", "seq_scan_cycles",
+                "seq_move_cycles", "seq_tail_cycles", "seq_rescans", "seq_entries",
+                "seq_queue_cycles", "seq_refresh_cycles", "seq_other_cycles", "seq_top2_cycles")
         return dict(zip(keys, (int(x) for x in out)))
 
     def launches(self):

@@ -100,9 +100,10 @@ struct crius_ctx {
   uint8_t *d_active = nullptr;
   double *d_total = nullptr;
   int64_t *d_round_stats = nullptr;
-  int32_t *d_list = nullptr;
-  AdmView adm_glob{};  // admitted-job records in global memory (only when they exceed shared)
-  EView eg{};          // (ii) move caches in global memory (rounds listing > kECap jobs)
+  int32_t *d_ao_pk = nullptr, *d_nao = nullptr, *d_rerr = nullptr, *d_ord = nullptr;
+  double *d_ao_sc = nullptr, *d_osc = nullptr;
+  uint64_t *d_gminb = nullptr, *d_tsb = nullptr;
+  AdmView adm_glob{};  // admitted-job records and type lists in global memory (beyond shared)
   int32_t round_policy = 0;  // crius_set_round_policy (NEXT-4 ablations)
   int64_t *d_tmax = nullptr;  // crius_set_deadline_bounds: [J] or unset
   bool has_tmax = false;
@@ -126,11 +127,11 @@ void free_all(crius_ctx *c) {
                   c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight,
                   c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
-                  c->d_rng, c->d_cur, c->d_free, c->d_total, c->eg.loss, c->eg.s2, c->eg.key, c->eg.T2,
-                  c->eg.i, c->eg.G2, c->eg.t2, c->d_round_stats, c->d_score, c->adm_glob.T, c->adm_glob.bi_T,
-                  c->adm_glob.sc, c->adm_glob.bi_key, c->adm_glob.bi_s, c->adm_glob.pos,
-                  c->adm_glob.cur, c->adm_glob.G, c->adm_glob.t, c->adm_glob.nopt,
-                  c->adm_glob.bi_opt, c->adm_glob.bi_G2, c->adm_glob.gmin, c->d_list,
+                  c->d_rng, c->d_cur, c->d_free, c->d_total, c->d_round_stats, c->d_score,
+                  c->d_ao_pk, c->d_nao, c->d_rerr, c->d_ord, c->d_ao_sc, c->d_osc, c->d_gminb, c->d_tsb,
+                  c->adm_glob.bk, c->adm_glob.ek, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
+                  c->adm_glob.t, c->adm_glob.slot, c->adm_glob.bi, c->adm_glob.ei, c->adm_glob.tl,
+                  c->adm_glob.gmb, c->adm_glob.tsb, c->adm_glob.nopt, c->adm_glob.po,
                   c->d_run_opt, c->d_cand, c->d_run_cell, c->d_active};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -144,7 +145,8 @@ struct JobSums {
 crius_status validate_static(const crius_cluster *cl, const crius_jobs *jb, const crius_config *cf,
                              int64_t *TL_out, int32_t *Lmax_out) {
   if (!cl || !jb || !cf) return fail(CRIUS_EINVAL, "null argument");
-  if (cl->n_types < 1 || cl->n_types > kMaxTypes) return fail(CRIUS_EINVAL, "n_types must be 1..16");
+  if (cl->n_types < 1 || cl->n_types > kRT)
+    return fail(CRIUS_EINVAL, "n_types must be 1..8 (the scheduling round's tables)");
   if (!cl->capacity || !cl->gpus_per_node || !cl->mem_bytes || !cl->alpha_intra_ns ||
       !cl->beta_intra_ns_per_mib || !cl->alpha_inter_ns || !cl->beta_inter_ns_per_mib)
     return fail(CRIUS_EINVAL, "null cluster array");
@@ -161,7 +163,8 @@ crius_status validate_static(const crius_cluster *cl, const crius_jobs *jb, cons
         cl->beta_inter_ns_per_mib[t] >= (int64_t(1) << 40))
       return fail(CRIUS_EINVAL, "beta out of range [0, 2^40) for type " + std::to_string(t));
   }
-  if (jb->n_jobs < 1) return fail(CRIUS_EINVAL, "n_jobs must be >= 1");
+  if (jb->n_jobs < 1 || jb->n_jobs >= (1 << 24))
+    return fail(CRIUS_EINVAL, "n_jobs must be in [1, 2^24) (the round's 24-bit priority tie keys)");
   if (jb->k_max < 0 || jb->k_max > kMaxKmax) return fail(CRIUS_EINVAL, "k_max must be 0..6");
   if (!jb->job_id || !jb->submit_time || !jb->n_gpus_req || !jb->global_batch || !jb->k_state ||
       !jb->n_layers || !jb->layer_off || !jb->compute_ns || !jb->param_bytes || !jb->act_bytes ||
@@ -912,30 +915,54 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int J = c->P.J, T = c->P.T;
-  if (T > kRT) return fail(CRIUS_EINVAL, "the scheduling round supports at most 8 GPU types");
   if (!c->d_opt) {
-    CK(dalloc(&c->d_opt, (size_t)J * c->maxopt));
-    CK(dalloc(&c->d_score, (size_t)J * c->maxopt));
-    CK(dalloc(&c->d_opt_cell, (size_t)J * c->maxopt));
+    const size_t JO = (size_t)J * c->maxopt;
+    CK(dalloc(&c->d_opt, JO));
+    CK(dalloc(&c->d_score, JO));
+    CK(dalloc(&c->d_opt_cell, JO));
+    CK(dalloc(&c->d_ao_pk, JO));
+    CK(dalloc(&c->d_ao_sc, JO));
     CK(dalloc(&c->d_ref, J));
     CK(dalloc(&c->d_decision, J));
     CK(dalloc(&c->d_nopt, J));
+    CK(dalloc(&c->d_nao, J));
+    CK(dalloc(&c->d_gminb, J));
+    CK(dalloc(&c->d_tsb, J));
     CK(dalloc(&c->d_rng, J));
     CK(dalloc(&c->d_cur, J));
     CK(dalloc(&c->d_free, 16));
     CK(dalloc(&c->d_total, 1));
-    CK(dalloc(&c->d_round_stats, 24));
+    CK(dalloc(&c->d_round_stats, 32));
     CK(dalloc(&c->d_run_opt, J));
     CK(dalloc(&c->d_cand, J));
     CK(dalloc(&c->d_run_cell, J));
     CK(dalloc(&c->d_active, J));
+    CK(dalloc(&c->d_rerr, 1));
+    CK(dalloc(&c->d_ord, J));
+    CK(dalloc(&c->d_osc, J));
+    // admitted records in global memory (used when they exceed shared memory)
+    CK(dalloc(&c->adm_glob.bk, J));
+    CK(dalloc(&c->adm_glob.ek, J));
+    CK(dalloc(&c->adm_glob.pos, J));
+    CK(dalloc(&c->adm_glob.cur, J));
+    CK(dalloc(&c->adm_glob.G, J));
+    CK(dalloc(&c->adm_glob.t, J));
+    CK(dalloc(&c->adm_glob.slot, J));
+    CK(dalloc(&c->adm_glob.bi, J));
+    CK(dalloc(&c->adm_glob.ei, J));
+    CK(dalloc(&c->adm_glob.gmb, J));
+    CK(dalloc(&c->adm_glob.tsb, J));
+    CK(dalloc(&c->adm_glob.nopt, J));
+    CK(dalloc(&c->adm_glob.po, J));
+    CK(dalloc(&c->adm_glob.tl, (size_t)T * J));
   }
   std::vector<int32_t> fr(T);
   for (int t = 0; t < T; ++t) {
     fr[t] = free_gpus ? free_gpus[t] : c->cap[t];
-    if (fr[t] < 0) return fail(CRIUS_EINVAL, "free_gpus must be >= 0");
+    if (fr[t] < 0 || fr[t] > (1 << 30)) return fail(CRIUS_EINVAL, "free_gpus must be in [0, 2^30]");
   }
   CK(cudaMemcpyAsync(c->d_free, fr.data(), T * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(c->d_rerr, 0, 4, st));
   if (run_cell) {
     for (int j = 0; j < J; ++j)
       if (run_cell[j] < -1 || run_cell[j] >= c->n_cells)
@@ -957,75 +984,50 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   R.opt_cell = c->d_opt_cell;
   R.nopt = c->d_nopt;
   R.ref = c->d_ref;
-  R.ng = c->d_rng;
   R.cur = c->d_cur;
   R.decision = c->d_decision;
   R.free_io = c->d_free;
   R.total = c->d_total;
   R.stats = c->d_round_stats;
+  R.ao_pk = c->d_ao_pk;
+  R.ao_sc = c->d_ao_sc;
+  R.nao = c->d_nao;
+  R.gminb = c->d_gminb;
+  R.tsb = c->d_tsb;
   R.run_cell = run_cell ? c->d_run_cell : nullptr;
   R.active = active ? c->d_active : nullptr;
   R.run_opt = c->d_run_opt;
   R.cand = c->d_cand;
+  R.err = c->d_rerr;
+  R.glob = c->adm_glob;
+  R.ord = c->d_ord;
+  R.osc = c->d_osc;
   k_round_options<<<(J + 127) / 128, 128, 0, st>>>(c->P, c->C.unit_cell_begin, c->C.type, c->C.G,
                                                    (const CellResult *)d_all, R);
   CKL();
-  // each admitted job holds >= 1 GPU: at most min(J, sum of free GPUs) records
-  int64_t max_adm = 0;
-  for (int t = 0; t < T; ++t) max_adm += fr[t];
-  if (run_cell)
-    for (int j = 0; j < J; ++j) max_adm += run_cell[j] >= 0;
-  max_adm = std::min<int64_t>(max_adm, J);
+  // K6 keeps the admitted records in dynamic shared memory when its own bound
+  // on their number fits (else global memory), and stages the admitted jobs'
+  // options in the rest (an option pool; jobs that find no room read the global
+  // table).  It gets the whole budget.
   cudaFuncAttributes fa{};
-  CK(cudaFuncGetAttributes(&fa, k_round_greedy));
+  CK(cudaFuncGetAttributes(&fa, k_round));
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-  const size_t budget = (size_t)optin - fa.sharedSizeBytes - 1024;  // dynamic next to static
-  const size_t per_job = (size_t)c->maxopt * (sizeof(OptRec) + 8) + 24;
-  int adm_in_smem = max_adm <= kAdmSmem;
-  size_t adm_bytes = adm_in_smem ? (size_t)kAdmSmem * kAdmBytes : 0;
-  if (adm_in_smem && (budget - adm_bytes) / per_job < 32) {
-    adm_in_smem = 0;
-    adm_bytes = 0;
-  }
-  int win_cap = (int)std::min<size_t>(256, (budget - adm_bytes) / per_job) & ~31;
-  if (win_cap < 32) return fail(CRIUS_EINVAL, "too many options per job for the round's window");
-  const size_t dsm = (size_t)win_cap * per_job + adm_bytes;
-  if (!adm_in_smem && !c->adm_glob.pos) {
-    CK(dalloc(&c->adm_glob.T, J));
-    CK(dalloc(&c->adm_glob.bi_T, J));
-    CK(dalloc(&c->adm_glob.sc, J));
-    CK(dalloc(&c->adm_glob.bi_key, J));
-    CK(dalloc(&c->adm_glob.bi_s, J));
-    CK(dalloc(&c->adm_glob.pos, J));
-    CK(dalloc(&c->adm_glob.cur, J));
-    CK(dalloc(&c->adm_glob.G, J));
-    CK(dalloc(&c->adm_glob.t, J));
-    CK(dalloc(&c->adm_glob.nopt, J));
-    CK(dalloc(&c->adm_glob.bi_opt, J));
-    CK(dalloc(&c->adm_glob.bi_G2, J));
-    CK(dalloc(&c->adm_glob.gmin, J));
-    CK(dalloc(&c->d_list, J));
-  }
-  if (!c->eg.i) {
-    CK(dalloc(&c->eg.loss, J));
-    CK(dalloc(&c->eg.s2, J));
-    CK(dalloc(&c->eg.key, J));
-    CK(dalloc(&c->eg.T2, J));
-    CK(dalloc(&c->eg.i, J));
-    CK(dalloc(&c->eg.G2, J));
-    CK(dalloc(&c->eg.t2, J));
-  }
-  R.eg = c->eg;
-  R.list = c->d_list;  // allocated above (global-record mode only)
-  CK(cudaFuncSetAttribute(k_round_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-  k_round_greedy<<<1, kRoundThreads, dsm, st>>>(R, adm_in_smem, c->adm_glob, win_cap);
+  size_t dsm = (size_t)optin - fa.sharedSizeBytes - 1024;
+  if (const char *cap = getenv("CRIUS_ROUND_SMEM")) dsm = std::min<size_t>(dsm, (size_t)atoll(cap));
+  R.smem_bytes = (int64_t)dsm;
+  CK(cudaFuncSetAttribute(k_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  k_round<<<1, kRoundThreads, dsm, st>>>(R);
   CKL();
   c->launches += 2;
+  int32_t rerr = 0;
   CK(cudaMemcpyAsync(decision, c->d_decision, (size_t)J * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(free_after, c->d_free, T * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(total_score, c->d_total, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&rerr, c->d_rerr, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (rerr == 1) return fail(CRIUS_EINVAL, "run_cell: a running Cell's (type, G) is not one of its job's options");
+  if (rerr == 2) return fail(CRIUS_EINVAL, "free + running GPUs of a type exceed 2^30");
   return CRIUS_OK;
 }
 
@@ -1056,7 +1058,7 @@ crius_status crius_round_stats(crius_ctx *c, int64_t *out16, void *stream) {
   if (!c->d_round_stats) return fail(CRIUS_ESTATE, "no round has run");
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemcpyAsync(out8, c->d_round_stats, 168, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out8, c->d_round_stats, 32 * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return CRIUS_OK;
 }

@@ -8,22 +8,32 @@
 //             G <= N_G, else ScaleResource with <= d victim moves
 //   Phase B = extra scheduling / reverse scaling, d sweeps
 //
-// K5 builds O_j for every job in priority order (one thread per job).
-// K6 is ONE CTA of 32 warps (the round is sequential by definition) that
-// extracts parallelism without changing the result:
-//  * speculative batches -- a job that stays pending changes no state, so 32
-//    consecutive jobs are evaluated at once (one per warp) against the same
-//    state; the first one that changes the state is committed and the next
-//    batch starts right after it: the exact sequential order of §N6;
-//  * ScaleResource tries the job's options in kappa order and stops at the
-//    first success; each option's success depends only on the state, so the
-//    lanes test all options at once and take the kappa-argmin of the successes;
-//  * the victim-move sequence of a trial depends only on the state and on the
-//    option's GPU type t_o (G_o only decides where it is cut), so the greedy
-//    sequence of every type is computed once per state and reused until an
-//    admission changes it: per-job caches of the best same-type move and of
-//    the best other-type move (staged options in shared memory), then one
-//    group of warps per type runs the d moves with one named barrier per move.
+// K5 builds O_j for every job in priority order (one thread per job), plus the
+// job's arrival options (G <= N_G) in kappa order, transposed [k][J] so that
+// one thread per job reads them coalesced.
+//
+// K6 is ONE CTA (the round is sequential by definition).  It evaluates the
+// literal §N6 order with three exact reformulations (DESIGN R-2):
+//  * speculative batches -- a job that stays pending changes no state, so the
+//    next kRoundThreads jobs are evaluated at once (one THREAD per job, its
+//    arrival options in kappa order: the first that fits is its direct choice)
+//    against the same state; the first job that is admitted is committed and
+//    the next batch starts right after it;
+//  * ScaleResource: the victim-move sequence of a trial depends only on the
+//    state and on the option's GPU type (G_o only decides where it is cut), so
+//    one greedy sequence per type serves every option of every pending job until
+//    an admission changes it.  From a type's sequence a table thr[t][log2 G]
+//    = the accumulated loss of the shortest prefix that frees G GPUs (or +inf)
+//    makes each option's trial one comparison score(o) > thr; the first success
+//    in kappa order is the job's ScaleResource outcome;
+//  * a type's sequence is computed by ONE warp over the type's admitted jobs
+//    (per-type lists): each job's best same-type move (case i) is cached and
+//    refreshed only when the job's option changes; its best other-type move
+//    (case ii) is computed only when one of its options on another type fits
+//    (exact test from per-type smallest-option bytes) and re-evaluated lazily
+//    when a move took the GPUs it needed (free' of the other types only
+//    decreases along a sequence).  Per move: one warp argmin over the lanes'
+//    best candidates, no block barrier.
 #pragma once
 #include "common.cuh"
 
@@ -35,23 +45,35 @@ struct OptRec {  // 16 B
   int32_t t;
 };
 
-// Cached best other-type move (case (ii)) of the listed jobs, entry k of the
-// list: the option with t2 != t and G2 <= free'[t2] of minimum loss = sc - s2
-// (ties -> lowest index); i = -1 if none.  Shared memory up to kECap entries.
-#ifndef CRIUS_ECAP
-#define CRIUS_ECAP 256
+constexpr int kRT = 8;  // GPU types supported by the round kernel (rejected at load beyond)
+#ifndef CRIUS_ROUND_THREADS
+#define CRIUS_ROUND_THREADS 256
 #endif
-constexpr int kECap = CRIUS_ECAP;
-struct EView {
-  double *loss, *s2, *key;  // key = loss / G_cur (the move's ScaleResource key)
-  int64_t *T2;
-  int32_t *i, *G2, *t2;
+constexpr int kRoundThreads = CRIUS_ROUND_THREADS;
+constexpr int kRoundWarps = kRoundThreads / 32;
+static_assert(kRoundWarps >= kRT && kRoundWarps <= 32, "one warp per GPU type, one ballot word per warp");
+constexpr int kLgMax = 31;  // G <= 2^30
+
+// Admitted jobs (SoA; shared memory when they fit, else global).  bi = cached
+// best same-type move (case i): option index | log2 G2 << 8; -2 stale (the
+// job's option changed), -1 none; bk its key.  ei = best other-type move
+// (case ii) under the sequence's current free': index | log2 G2 << 8 | t2 << 16,
+// -1 none; ek its key.  slot = position in its type's list tl.
+struct AdmView {
+  double *bk, *ek;
+  uint64_t *gmb, *tsb;  // the job's gminb / tsb bytes (see RoundBuf)
+  int32_t *pos, *cur, *G, *t, *slot, *bi, *ei, *nopt;
+  int32_t *po;  // offset of the job's options in the shared-memory pool, -1 = not staged
+  int32_t *tl;  // per-type lists of admitted records, type u at tl + toff[u]
+  double *psc;  // option pool (shared memory): scores
+  int32_t *ppk; //   and log2 G | t << 8
 };
 
 struct RoundBuf {
   int32_t J, T, maxopt, depth;
   int32_t policy;        // NEXT-4 ablations (R-11): bit 0 NA (options at G = N_G only),
                          // bit 1 NH (admitted jobs keep their GPU type)
+  int64_t smem_bytes;    // dynamic shared memory for the admitted records and type lists
   const int64_t *tmax;   // [J] by job or NULL: deadline bound on an option's T (R-12)
   const int32_t *rank;   // [J] job -> priority position
   const int32_t *pi;     // [J] position -> job
@@ -60,27 +82,43 @@ struct RoundBuf {
   int64_t *opt_cell;     // [J][maxopt]
   int32_t *nopt;         // [J] by position
   int64_t *ref;          // [J] by position (kInf = unschedulable)
-  int32_t *ng;           // [J] by position
-  int32_t *cur;          // [J] by position: option index or -1
+  int32_t *cur;          // [J] by position: option index or -1 (written at the end)
   int64_t *decision;     // [J] by job
   int32_t *free_io;      // [T]
   double *total;
-  int64_t *stats;        // [16] counters (see crius_round_stats)
-  int32_t *list;         // [J] scratch list (used when admitted records live in global memory)
+  int64_t *stats;        // [24] counters (see crius_round_stats)
+  // arrival options (G <= N_G) in kappa order, transposed: entry k of position
+  // p at [k * J + p]; pk = option index | log2 G << 8 | t << 13
+  int32_t *ao_pk;
+  double *ao_sc;
+  int32_t *nao;          // [J] by position
+  uint64_t *gminb;       // [J] byte u = log2 of the job's smallest option G on type u (0xff none)
+  uint64_t *tsb;         // [J] byte u = index of the job's first option on type u
   // NEXT-4 round state (NULL = every job active, none running)
   const int64_t *run_cell;  // [J] by job: Cell the job runs on, or -1
   const uint8_t *active;    // [J] by job: the job takes part in this round
   int32_t *run_opt;         // [J] by position: option index of the running Cell, or -1
   int8_t *cand;             // [J] by position: 1 = Phase A candidate (active, not running)
-  EView eg;                 // [J] (ii) caches when more than kECap jobs are listed
+  int32_t *err;             // [1] 0 ok; 1 = a running Cell is not one of its job's options;
+                            // 2 = free + running GPUs of a type exceed 2^30
+  AdmView glob;             // records [J] and type lists [T * J] in global memory
+  int32_t *ord;             // [J] scratch: admitted records in priority order
+  double *osc;              // [J] scratch: their scores
 };
 
 __device__ __forceinline__ double score_of(int64_t ref, int64_t T) {
   return __ddiv_rn((double)ref, (double)T);
 }
 
+__device__ __forceinline__ bool kappa_less(const OptRec &a, const OptRec &b) {
+  if (a.T != b.T) return a.T < b.T;
+  if (a.G != b.G) return a.G < b.G;
+  return a.t < b.t;
+}
+
 // K5: per job (thread), options, ref and scores from its Cells (contiguous,
-// (t, G, S) order), written at the job's priority position.
+// (t, G, S) order), written at the job's priority position; the arrival
+// options in kappa order; per-type smallest G and first index.
 __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
                                 const int32_t *__restrict__ cType, const int32_t *__restrict__ cG,
                                 const CellResult *__restrict__ res, RoundBuf R) {
@@ -94,8 +132,8 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
   int n = 0;
   int64_t ref_ng = kInf, ref_any = kInf;
   int lastT = -1, lastG = -1;
-  const bool act0 = R.active ? R.active[j] != 0 : true;
-  const int64_t rc0 = (act0 && R.run_cell) ? R.run_cell[j] : -1;
+  const bool act = R.active ? R.active[j] != 0 : true;
+  const int64_t rc0 = (act && R.run_cell) ? R.run_cell[j] : -1;
   const int64_t tmx = R.tmax ? R.tmax[j] : kInf;
   for (int64_t c = c0; c < c1; ++c) {
     const int64_t T = res[c].t_ns;
@@ -124,127 +162,46 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
   }
   const int64_t ref = ref_ng != kInf ? ref_ng : ref_any;
   double *sc = R.score + (int64_t)pos * R.maxopt;
-  for (int i = 0; i < n; ++i) sc[i] = score_of(ref, o[i].T);
+  uint64_t gmb = ~0ull, tsv = ~0ull;
+  for (int i = 0; i < n; ++i) {
+    sc[i] = score_of(ref, o[i].T);
+    const int sh = 8 * o[i].t;
+    if (((gmb >> sh) & 0xff) == 0xff) {  // first (smallest G) option of its type
+      gmb = (gmb & ~(0xffull << sh)) | ((uint64_t)ilog2_pow2((uint32_t)o[i].G) << sh);
+      tsv = (tsv & ~(0xffull << sh)) | ((uint64_t)i << sh);
+    }
+  }
+  R.gminb[pos] = gmb;
+  R.tsb[pos] = tsv;
+  // arrival options (G <= N_G) in kappa order: rank by counting
+  int na = 0;
+  for (int i = 0; i < n; ++i) {
+    const OptRec x = o[i];
+    if (x.G > ngj) continue;
+    int r = 0;
+    for (int i2 = 0; i2 < n; ++i2) {
+      const OptRec y = o[i2];
+      r += (y.G <= ngj && kappa_less(y, x));
+    }
+    R.ao_pk[(int64_t)r * R.J + pos] = i | (ilog2_pow2((uint32_t)x.G) << 8) | (x.t << 13);
+    R.ao_sc[(int64_t)r * R.J + pos] = sc[i];
+    ++na;
+  }
+  R.nao[pos] = na;
   R.nopt[pos] = n;
   R.ref[pos] = ref;
-  R.ng[pos] = ngj;
   R.cur[pos] = -1;
   // round state: a running job keeps the option of its Cell's (type, G)
-  const bool act = R.active ? R.active[j] != 0 : true;
   int ro = -1;
   if (act && R.run_cell && R.run_cell[j] >= 0) {
     const int64_t rc = R.run_cell[j];
     for (int i = 0; i < n; ++i)
       if (o[i].t == cType[rc] && o[i].G == cG[rc]) ro = i;
-    CRIUS_CHECK(ro >= 0);
+    if (ro < 0) atomicExch(R.err, 1);  // the oracle rejects this input (status 2)
   }
   R.run_opt[pos] = ro;
-  R.cand[pos] = (int8_t)(act && ro < 0 && ref != kInf);
+  R.cand[pos] = (int8_t)(act && ro < 0 && ref != kInf && na > 0);
 }
-
-// Option records are read-only inside K6: load them through the non-coherent
-// (L1-cached) path so repeated scans of the same admitted jobs hit L1.
-__device__ __forceinline__ OptRec ldg_opt(const OptRec *p) {
-  const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(p));
-  OptRec r;
-  r.T = v.x;
-  r.G = (int32_t)(v.y & 0xffffffff);
-  r.t = (int32_t)(v.y >> 32);
-  return r;
-}
-
-__device__ __forceinline__ bool kappa_less(const OptRec &a, const OptRec &b) {
-  if (a.T != b.T) return a.T < b.T;
-  if (a.G != b.G) return a.G < b.G;
-  return a.t < b.t;
-}
-
-constexpr int kRoundThreads = 1024;
-constexpr int kRT = 8;  // GPU types supported by the round kernel (shared-memory tables)
-constexpr int kRoundWarps = kRoundThreads / 32;
-#ifndef CRIUS_ADM_SMEM
-#define CRIUS_ADM_SMEM 2048
-#endif
-constexpr int kAdmSmem = CRIUS_ADM_SMEM;  // admitted-job records kept in shared memory up to this many
-constexpr int kAdmBytes = 76;   // bytes per admitted-job record (incl. scratch list)
-
-// Other-type options of the listed jobs, staged in shared memory by the warp
-// that fills their entry (po[k] = offset, pn[k] = count, -1 = not staged:
-// refills then re-read the options from global memory).
-#ifndef CRIUS_POOL
-#define CRIUS_POOL 512
-#endif
-constexpr int kPool = CRIUS_POOL;
-struct OptPool {
-  int64_t *T2;
-  double *s2;
-  int32_t *G2, *ti;  // ti = t2 << 8 | option index
-  int32_t *po, *pn;
-  int32_t *used;
-};
-
-// Admitted jobs, in priority order (SoA; shared memory when they fit, else global).
-// bi_* caches the job's best same-type victim move (case (i) of ScaleResource),
-// which depends only on its current option: bi_opt = -2 marks a stale cache
-// (set whenever the option changes), -1 = no such move.  gmin = the job's
-// smallest option G (an other-type move (ii) needs G_o' <= free'[t_o']).
-struct AdmView {
-  int64_t *T, *bi_T;
-  double *sc, *bi_key, *bi_s;
-  int32_t *pos, *cur, *G, *t, *nopt, *bi_opt, *bi_G2, *gmin;
-};
-
-// Window of upcoming jobs (priority positions [w0, w0 + wn)) staged in shared memory.
-struct JobWin {
-  int64_t *ref;
-  int32_t *nopt, *ng;
-  int8_t *cand;
-  OptRec *opt;
-  double *score;
-  int cap, w0, wn;
-};
-
-struct RoundShared {
-  int32_t fr[kRT];
-  int32_t n_adm, advance, any_change, n_dirty, n_list, n_invalid;
-  // per-type sequence validity: a sequence is reused until a job of its type
-  // changes or a changed free count could admit an other-type move of one of its
-  // jobs (gmin_type = smallest option G over its jobs, a conservative bound)
-  int32_t seq_ok[kRT], comp[kRT], gmin_type[kRT];
-  int32_t fr_base[kRT][kRT];  // free counts the sequence was computed from
-  int32_t old_fr[kRT];        // free counts before the current commit (thread 0)
-  uint32_t changed;           // types changed by the current commit; 0 = no commit
-  long long prof[12];  // cycles: [0] setup+dirty, [1] listing, [2] (ii) caches, [3] sequences; [4] dirty jobs, [5] listed jobs
-  // victim-move sequences, one per GPU type, cut at <= d moves
-  int32_t len[kRT];
-  int32_t mv_a[kRT][kMaxDepth], mv_opt[kRT][kMaxDepth];
-  int32_t mv_G[kRT][kMaxDepth], mv_t[kRT][kMaxDepth];  // the victim's new option
-  int64_t mv_T[kRT][kMaxDepth];
-  double mv_sc[kRT][kMaxDepth];
-  double cum[kRT][kMaxDepth + 1];                 // ((0 + loss_1) + loss_2) + ...
-  int32_t frs[kRT][kMaxDepth + 1][kRT];      // free' after m moves
-  int32_t fmax_other[kRT];                         // max_{t2 != t} free'[t2]
-  // per-warp outcome of one speculative batch
-  int32_t res_kind[kRoundWarps], res_opt[kRoundWarps], res_m[kRoundWarps], need[kRoundWarps];
-  int32_t res_G[kRoundWarps], res_t[kRoundWarps];
-  int64_t res_T[kRoundWarps];
-  double res_sc[kRoundWarps];
-  // per-warp best move of the current sequence step (type groups of warps,
-  // double-buffered by move parity), each warp's free' and moved jobs
-  double g_key[2][kRoundWarps];
-  uint32_t g_tie[2][kRoundWarps];
-  int32_t g_a[2][kRoundWarps], g_idx[2][kRoundWarps], g_G2[2][kRoundWarps];
-  int32_t g_t2o[2][kRoundWarps], g_freed[2][kRoundWarps];
-  int32_t wf2[kRoundWarps][kRT], wmv[kRoundWarps][kMaxDepth];
-  // cached best other-type moves of the listed jobs (EView, up to kECap)
-  double e_loss[kECap], e_s2[kECap], e_key[kECap];
-  int64_t e_T2[kECap];
-  int32_t e_i[kECap], e_G2[kECap], e_t2[kECap], e_po[kECap], e_pn[kECap];
-  // their other-type options (OptPool)
-  int64_t p_T2[kPool];
-  double p_s2[kPool];
-  int32_t p_G2[kPool], p_ti[kPool], p_used;
-};
 
 // ---- warp argmin by lexicographic 3-word keys, one redux.sync per word ------
 // Order-preserving u64 image of a double (no NaN; -0.0 normalised to +0.0).
@@ -275,412 +232,566 @@ __device__ __forceinline__ uint32_t kappa_tie(const OptRec &x) {
   return ((uint32_t)ilog2_pow2((uint32_t)x.G) << 8) | (uint32_t)x.t;
 }
 
-// Warp: refresh the same-type move cache (case (i)) and gmin of admitted job a.
-// The cached move is the job's argmin of key = loss / freed over its same-type
-// options with smaller G, ties -> lowest option index.  Lanes cover the job's
-// options (coalesced 16-byte records and their scores, one round trip).
-__device__ __forceinline__ void refresh_victim_cache(const RoundBuf &R, const AdmView &A, int a) {
-  const int lane = threadIdx.x & 31;
-  const int v = A.pos[a], cv = A.cur[a], Gc = A.G[a], t = A.t[a], nv = A.nopt[a];
-  const double sc = A.sc[a];
-  bool have = false;
-  double bk = 0.0, bs = 0.0;
-  int bi = 0, bG = 0;
-  int64_t bT = 0;
-  int gmin = INT32_MAX;
-  for (int i2 = lane; i2 < nv; i2 += 32) {
-    const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
-    const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
-    gmin = min(gmin, o2.G);
-    if (i2 == cv || o2.t != t || o2.G >= Gc) continue;
-    const double k = __ddiv_rn(sc - s2, (double)(Gc - o2.G));
-    if (!have || k < bk) {  // i2 ascending per lane: ties keep the lower index
-      have = true;
+__device__ __forceinline__ OptRec ldg_opt(const OptRec *p) {
+  const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(p));
+  OptRec r;
+  r.T = v.x;
+  r.G = (int32_t)(v.y & 0xffffffff);
+  r.t = (int32_t)(v.y >> 32);
+  return r;
+}
+
+__device__ __forceinline__ int byte_of(uint64_t v, int u) { return (int)((v >> (8 * u)) & 0xff); }
+
+// One victim-move sequence per GPU type and the ScaleResource thresholds.
+constexpr int kTop = 32;      // same-type move candidates kept sorted per type (lane = entry)
+constexpr int kTopFill = 16;  // entries a refill selects
+constexpr int kQ = 64;        // other-type evaluation queue of a type warp
+struct SeqTab {
+  int32_t len;
+  int32_t mv_a[kMaxDepth];   // victim (admitted record)
+  int32_t mv_pk[kMaxDepth];  // its new option: index | log2 G2 << 8 | t2 << 16
+  int32_t dfr[kMaxDepth + 1][kRT];  // free-count deltas after m moves
+  double cum[kMaxDepth + 1];        // ((0 + loss_1) + loss_2) + ...
+  double thr[kLgMax];               // accumulated loss of the shortest prefix freeing 2^lg, or +inf
+  int8_t thm[kLgMax];               // that prefix's length
+  int32_t f2[kRT];                  // the type warp's working free'
+  uint64_t gq;  // byte u <= log2 of the smallest option G on type u over the type's jobs (a lower
+                // bound: records only join a type's bound, never leave it -- conservative)
+  // top list: the tcnt smallest same-type (case i) candidates of the type's
+  // jobs, ascending by (key, priority, option); tall = it holds all of them
+  double tk[kTop];
+  uint32_t tt[kTop];
+  int32_t ta[kTop], tp[kTop];
+  int32_t tcnt, tall;
+  int32_t qd[kQ], ql[kQ];  // work queues of the type warp
+};
+
+struct RoundShared {
+  int32_t fr[kRT], old_fr[kRT];
+  int32_t toff[kRT + 1], tn[kRT];
+  unsigned long long tcap[kRT];  // free + GPUs held by running jobs, per type
+  int32_t n_adm, advance, any_change, lo;
+  int32_t p_used, p_cap;     // option pool entries used / available
+  int32_t po_first;          // pool offset of the first record of the current commit
+  int32_t dmark;             // records [dmark, n_adm) were admitted since the last recompute
+  int32_t n_vic, vic[kMaxDepth];  // records moved by the commit since the last recompute
+  uint32_t changed;
+  uint32_t stale;            // types whose sequence must be recomputed
+  SeqTab sq[kRT];
+  uint32_t wk1[kRoundWarps], wnd[kRoundWarps], wk2[kRoundWarps];
+  int32_t res[kRoundThreads];  // per job of the batch: option index | log2 G << 8 | t << 13 | m << 16
+  uint64_t bs_gmb[kRoundThreads], bs_tsb[kRoundThreads];  // per job of the batch, for its record
+  int32_t bs_nopt[kRoundThreads];
+  int32_t wsum[kRoundWarps];
+  long long prof[8], prof2[8];
+  int32_t cnt[8];
+};
+
+// ---- type lists -------------------------------------------------------------
+__device__ __forceinline__ void list_remove(RoundShared &sh, const AdmView &A, int a) {
+  const int u = A.t[a], s = A.slot[a];
+  int32_t *tl = A.tl + sh.toff[u];
+  const int last = tl[--sh.tn[u]];
+  tl[s] = last;
+  A.slot[last] = s;
+}
+__device__ __forceinline__ void list_add(RoundShared &sh, const AdmView &A, int a, int u) {
+  int32_t *tl = A.tl + sh.toff[u];
+  const int s = sh.tn[u]++;
+  tl[s] = a;
+  A.slot[a] = s;
+}
+
+// Option i of admitted record a: (log2 G | t << 8) and its score, from the
+// shared-memory pool when the record's options were staged there (po >= 0),
+// else from the global option table.
+__device__ __forceinline__ void opt_get(const RoundBuf &R, const AdmView &A, int po, int p, int i,
+                                        int &lg, int &t, double &s) {
+  if (po >= 0) {
+    const int pk = A.ppk[po + i];
+    lg = pk & 0xff;
+    t = pk >> 8;
+    s = A.psc[po + i];
+  } else {
+    const OptRec o = ldg_opt(R.opt + (int64_t)p * R.maxopt + i);
+    lg = ilog2_pow2((uint32_t)o.G);
+    t = o.t;
+    s = __ldg(R.score + (int64_t)p * R.maxopt + i);
+  }
+}
+
+// One lane: the job's best same-type move (case i): argmin over its options on
+// its type with smaller G (indices [first of type, cur) in (t, G) order) of
+// key = (score(cur) - score(o')) / (G_cur - G_o'), ties -> lowest index.
+__device__ __forceinline__ void refresh_i(const RoundBuf &R, const AdmView &A, int a) {
+  const int p = A.pos[a], cv = A.cur[a], Gc = A.G[a], tt = A.t[a], po = A.po[a];
+  const int i0 = byte_of(A.tsb[a], tt);
+  int lg, t2;
+  double sc;
+  opt_get(R, A, po, p, cv, lg, t2, sc);
+  int bi = -1;
+  double bk = 0.0;
+#pragma unroll 4
+  for (int i2 = i0; i2 < cv; ++i2) {  // ascending: strict < keeps the lowest index on ties
+    double s2;
+    opt_get(R, A, po, p, i2, lg, t2, s2);
+    const double k = __ddiv_rn(__dsub_rn(sc, s2), (double)(Gc - (1 << lg)));
+    if (bi < 0 || k < bk) {
+      bi = i2 | (lg << 8);
       bk = k;
-      bs = s2;
-      bi = i2;
-      bG = o2.G;
-      bT = o2.T;
     }
   }
-  gmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)gmin);
-  const int src = warp_lex_argmin(have, ord_double(bk), (uint32_t)bi);
-  if (src < 0) {
-    if (lane == 0) A.bi_opt[a] = -1;
-  } else if (lane == src) {
-    A.bi_opt[a] = bi;
-    A.bi_key[a] = bk;
-    A.bi_G2[a] = bG;
-    A.bi_T[a] = bT;
-    A.bi_s[a] = bs;
-  }
-  if (lane == 0) A.gmin[a] = gmin;
+  A.bi[a] = bi;
+  A.bk[a] = bk;
 }
 
-// Warp: fill entry k for admitted job a under free' = f2 (lanes over options)
-// and stage the job's other-type options in the pool when it has room.
-__device__ __forceinline__ void other_type_best_warp(const RoundBuf &R, const AdmView &A, int a,
-                                                     const int32_t *f2, const EView &E, int k,
-                                                     const OptPool *pool) {
-  const int lane = threadIdx.x & 31;
-  const int v = A.pos[a], t = A.t[a], nv = A.nopt[a];
-  const double sc = A.sc[a];
-  int off = -1;
-  if (pool) {
-    if (lane == 0) {
-      off = atomicAdd(pool->used, nv);
-      if (off + nv > kPool) off = -1;
-    }
-    off = __shfl_sync(0xffffffffu, off, 0);
-  }
-  int cnt = 0;
-  bool have = false;
-  double bl = 0.0, bs = 0.0;
-  int bi = 0, bG = 0, bt = 0;
-  int64_t bT = 0;
-  for (int i0 = 0; i0 < nv; i0 += 32) {
-    const int i2 = i0 + lane;
-    OptRec o2{0, 0, t};
-    double s2 = 0.0;
-    if (i2 < nv) {
-      o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
-      s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
-    }
-    const bool oth = i2 < nv && o2.t != t;
-    if (off >= 0) {
-      const unsigned bm = __ballot_sync(0xffffffffu, oth);
-      if (oth) {
-        const int q = off + cnt + __popc(bm & ((1u << lane) - 1));
-        pool->T2[q] = o2.T;
-        pool->s2[q] = s2;
-        pool->G2[q] = o2.G;
-        pool->ti[q] = (o2.t << 8) | i2;
-      }
-      cnt += __popc(bm);
-    }
-    if (!oth || o2.G > f2[o2.t]) continue;
-    const double l = sc - s2;
-    if (!have || l < bl) {
-      have = true;
-      bl = l;
-      bs = s2;
-      bi = i2;
-      bG = o2.G;
-      bt = o2.t;
-      bT = o2.T;
-    }
-  }
-  if (pool && lane == 0) {
-    pool->po[k] = off;
-    pool->pn[k] = cnt;
-  }
-  const int src = warp_lex_argmin(have, ord_double(bl), (uint32_t)bi);
-  if (src < 0) {
-    if (lane == 0) E.i[k] = -1;
-  } else if (lane == src) {
-    E.i[k] = bi;
-    E.loss[k] = bl;
-    E.key[k] = __ddiv_rn(bl, (double)A.G[a]);
-    E.s2[k] = bs;
-    E.G2[k] = bG;
-    E.t2[k] = bt;
-    E.T2[k] = bT;
-  }
-}
-
-// One lane: recompute entry k after a (ii) move took GPUs its option needed
-// (free' only decreases for the other types along a sequence); options from
-// the pool (shared memory) when staged, else from global memory.
-__device__ __forceinline__ int other_type_best_lane(const RoundBuf &R, const AdmView &A, int a,
-                                                    const int32_t *f2, const EView &E, int k,
-                                                    const OptPool *pool) {
-  const double sc = A.sc[a];
+// One lane: the job's best other-type move (case ii) under free' = f2: argmin
+// over its options on other types with G2 <= f2[t2] of loss = score(cur) -
+// score(o'), ties -> lowest index; key = loss / G_cur (exact: G_cur is a power
+// of two).  Returns the packed move or -1.
+__device__ __forceinline__ int compute_ii(const RoundBuf &R, const AdmView &A, int a,
+                                          const int32_t *f2) {
+  const int p = A.pos[a], cv = A.cur[a], tt = A.t[a], Gc = A.G[a], po = A.po[a];
+  const int nv = A.nopt[a];
+  int lg, t2;
+  double sc;
+  opt_get(R, A, po, p, cv, lg, t2, sc);
   int bi = -1;
   double bl = 0.0;
-  const int off = pool ? pool->po[k] : -1;
-  if (off >= 0) {  // other-type options in index order
-    const int n = pool->pn[k];
-    int bq = -1;
-    for (int q = off; q < off + n; ++q) {
-      const int ti = pool->ti[q], G2 = pool->G2[q];
-      if (G2 > f2[ti >> 8]) continue;
-      const double l = sc - pool->s2[q];
-      if (bi < 0 || l < bl) {
-        bi = ti & 0xff;
-        bl = l;
-        bq = q;
-      }
-    }
-    if (bq >= 0) {
-      E.loss[k] = bl;
-      E.key[k] = __ddiv_rn(bl, (double)A.G[a]);
-      E.s2[k] = pool->s2[bq];
-      E.G2[k] = pool->G2[bq];
-      E.t2[k] = pool->ti[bq] >> 8;
-      E.T2[k] = pool->T2[bq];
-    }
-    E.i[k] = bi;
-    return bi;
-  }
-  const int v = A.pos[a], t = A.t[a], nv = A.nopt[a];
 #pragma unroll 4
   for (int i2 = 0; i2 < nv; ++i2) {
-    const OptRec o2 = ldg_opt(R.opt + (int64_t)v * R.maxopt + i2);
-    const double s2 = __ldg(R.score + (int64_t)v * R.maxopt + i2);
-    if (o2.t == t || o2.G > f2[o2.t]) continue;
-    const double l = sc - s2;
+    double s2;
+    opt_get(R, A, po, p, i2, lg, t2, s2);
+    if (t2 == tt || (1 << lg) > f2[t2]) continue;
+    const double l = __dsub_rn(sc, s2);
     if (bi < 0 || l < bl) {
-      bi = i2;
+      bi = i2 | (lg << 8) | (t2 << 16);
       bl = l;
-      E.loss[k] = l;
-      E.s2[k] = s2;
-      E.G2[k] = o2.G;
-      E.t2[k] = o2.t;
-      E.T2[k] = o2.T;
     }
   }
-  if (bi >= 0) E.key[k] = __ddiv_rn(bl, (double)A.G[a]);
-  E.i[k] = bi;
+  A.ei[a] = bi;
+  if (bi >= 0) A.ek[a] = __ddiv_rn(bl, (double)Gc);
   return bi;
 }
 
-__device__ __forceinline__ void group_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+// A lane's candidate move.
+struct Cand {
+  double key;
+  uint32_t tie;  // priority position << 8 | option index
+  int a, pk;     // record, packed new option (index | log2 G2 << 8 | t2 << 16)
+  bool have;
+};
+
+__device__ __forceinline__ bool key_less(double k, uint32_t tie, double k2, uint32_t tie2) {
+  return k < k2 || (k == k2 && tie < tie2);
+}
+__device__ __forceinline__ bool cand_less(double k, uint32_t tie, const Cand &b) {
+  return !b.have || key_less(k, tie, b.key, b.tie);
 }
 
-// Warps [t*gw, (t+1)*gw): the greedy victim sequence of GPU type t (the §N6
-// ScaleResource move loop run for d moves without the G_o stop; an option on
-// type t later uses the shortest prefix that frees G_o).  Per move, the argmin
-// of (key, priority position, option) over the unmoved type-t jobs' cached
-// same-type moves (i) and the listed jobs' cached other-type moves (ii),
-// key = loss / freed.  One named barrier (1 + t) per move: every warp reduces
-// the group's per-warp winners itself (slots double-buffered by move parity)
-// and keeps its own copy of free' and of the moved jobs; the group's first
-// warp records the sequence.
-__device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView &A,
-                              const int32_t *list, int nE, const EView &E, const OptPool *pool,
-                              int t, int gw) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int gwid = wid - t * gw, gt = gwid * 32 + lane, gn = gw * 32, w0 = t * gw;
-  const int n_adm = sh.n_adm, TT = R.T;
-  int32_t *f2 = sh.wf2[wid];
-  int32_t *mv = sh.wmv[wid];
-  if (lane < TT) f2[lane] = sh.frs[t][0][lane];
-  __syncwarp();
-  // each thread's best cached same-type move (i) over its strided jobs only
-  // changes when that job is moved: rescan only then
-  bool hv1 = false;
-  double bk1 = 0.0;
-  int bp1 = 0, bi1 = 0, ba1 = -1;
-  bool rescan = true;
-  for (int m = 0; m < R.depth; ++m) {
-    if (rescan) {
-      hv1 = false;
-      ba1 = -1;
-      for (int a = gt; a < n_adm; a += gn) {  // (i): loads issued together
-        const int ta = A.t[a], bo = A.bi_opt[a], p = A.pos[a];
-        const double k = A.bi_key[a];
-        bool moved = false;
-        for (int q = 0; q < m; ++q) moved |= mv[q] == a;
-        if (ta != t || bo < 0 || moved) continue;
-        if (!hv1 || k < bk1 || (k == bk1 && (p < bp1 || (p == bp1 && bo < bi1)))) {
-          hv1 = true;
-          bk1 = k;
-          bp1 = p;
-          bi1 = bo;
-          ba1 = a;
-        }
-      }
+__device__ __forceinline__ bool ii_fits(int pk, const int32_t *f2) {
+  return (1 << ((pk >> 8) & 0xff)) <= f2[(pk >> 16) & 0xff];
+}
+
+// Record a's cached other-type move as a candidate (none if ei < 0).
+__device__ __forceinline__ Cand ii_cand(const AdmView &A, int a, int ei) {
+  Cand c;
+  c.have = ei >= 0;
+  if (c.have) {
+    c.key = A.ek[a];
+    c.tie = ((uint32_t)A.pos[a] << 8) | (ei & 0xff);
+    c.a = a;
+    c.pk = ei;
+  }
+  return c;
+}
+
+// Keep the lane's two best candidates (distinct records).
+__device__ __forceinline__ void top2_take(Cand &b1, Cand &b2, const Cand &c) {
+  if (!c.have) return;
+  if (cand_less(c.key, c.tie, b1)) {
+    b2 = b1;
+    b1 = c;
+  } else if (cand_less(c.key, c.tie, b2)) {
+    b2 = c;
+  }
+}
+
+// The type warp's top list in registers: lane i holds entry i.
+struct TopLane {
+  double k;
+  uint32_t tie;
+  int a, pk;
+};
+
+__device__ __forceinline__ TopLane top_shfl(const TopLane &x, int src) {
+  TopLane y;
+  y.k = __shfl_sync(0xffffffffu, x.k, src);
+  y.tie = __shfl_sync(0xffffffffu, x.tie, src);
+  y.a = __shfl_sync(0xffffffffu, x.a, src);
+  y.pk = __shfl_sync(0xffffffffu, x.pk, src);
+  return y;
+}
+
+// Insert candidate c into the sorted top list (cnt entries) if it belongs to
+// the prefix the list represents: always when the list holds every candidate,
+// else only below its last entry.  A full list drops its last entry.
+__device__ __forceinline__ void top_insert(TopLane &x, int &cnt, bool &all, const TopLane &c) {
+  const int lane = threadIdx.x & 31;
+  if (!all) {
+    if (cnt == 0) return;
+    const double lk = __shfl_sync(0xffffffffu, x.k, cnt - 1);
+    const uint32_t lt = __shfl_sync(0xffffffffu, x.tie, cnt - 1);
+    if (!key_less(c.k, c.tie, lk, lt)) return;
+  }
+  const int p = __popc(__ballot_sync(0xffffffffu, lane < cnt && key_less(x.k, x.tie, c.k, c.tie)));
+  const TopLane up = top_shfl(x, max(lane - 1, 0));
+  if (lane > p) x = up;
+  if (lane == p) x = c;
+  if (cnt == kTop) all = false;  // the old last entry dropped out
+  cnt = min(cnt + 1, kTop);
+}
+
+// Warp t: refill the top list with the kTopFill smallest same-type candidates
+// of type t (every record of the type has a fresh cache).  Each lane keeps a
+// sorted run of its records' 4 smallest; the warp pops the global minimum.
+__device__ __noinline__ void top_refill(const RoundShared &sh, const AdmView &A, int t, TopLane &x,
+                                        int &cnt, bool &all) {
+  const int lane = threadIdx.x & 31;
+  const int n_t = sh.tn[t];
+  const int32_t *tl = A.tl + sh.toff[t];
+  constexpr int kL = 4;
+  TopLane loc[kL];
+  int nloc = 0, nmine = 0;
+  // after the first pass a lane only takes candidates above the last one popped from it
+  double lk = 0.0;
+  uint32_t lt = 0;
+  bool first = true;
+  auto fill = [&]() {
+    nloc = 0;
+    for (int k = lane; k < n_t; k += 32) {
+      const int a = tl[k], bi = A.bi[a];
+      if (bi < 0) continue;
+      const TopLane c{A.bk[a], ((uint32_t)A.pos[a] << 8) | (bi & 0xff), a, bi | (t << 16)};
+      if (first) ++nmine;
+      else if (!key_less(lk, lt, c.k, c.tie)) continue;
+      int pos = 0;
+#pragma unroll
+      for (int q = 0; q < kL; ++q) pos += (q < nloc && key_less(loc[q].k, loc[q].tie, c.k, c.tie));
+      if (pos >= kL) continue;
+#pragma unroll
+      for (int q = kL - 1; q > 0; --q)
+        if (q > pos) loc[q] = loc[q - 1];
+#pragma unroll
+      for (int q = 0; q < kL; ++q)
+        if (q == pos) loc[q] = c;
+      nloc = min(nloc + 1, kL);
     }
-    bool have = hv1;
-    double bk = bk1;
-    int bp = bp1, bi = bi1, ba = ba1, bidx = -1;
-    for (int k = gt; k < nE; k += gn) {  // (ii)
-      const int a = list[k];
-      const int ta = A.t[a], p = A.pos[a], G2 = E.G2[k], t2 = E.t2[k];
-      int ei = E.i[k];
-      double key = E.key[k];
-      bool moved = false;
-      for (int q = 0; q < m; ++q) moved |= mv[q] == a;
-      if (ta != t || moved) continue;
-      if (ei >= 0 && G2 > f2[t2]) {
-        ei = other_type_best_lane(R, A, a, f2, E, k, pool);
-        key = E.key[k];
-      }
-      if (ei < 0) continue;
-      if (!have || key < bk || (key == bk && (p < bp || (p == bp && ei < bi)))) {
-        have = true;
-        bk = key;
-        bp = p;
-        bi = ei;
-        ba = a;
-        bidx = k;
-      }
-    }
-    const uint32_t tie = ((uint32_t)bp << 8) | (uint32_t)bi;
-    const int src = warp_lex_argmin(have, ord_double(bk), tie);
-    const int par = m & 1;
-    if (lane == 0) sh.g_a[par][wid] = -1;
-    __syncwarp();
+  };
+  fill();
+  first = false;
+  int left = nmine;  // this lane's candidates not yet popped
+  const int total = __reduce_add_sync(0xffffffffu, nmine);
+  const int want = min(kTopFill, total);
+  for (int i = 0; i < want; ++i) {
+    const bool hv = nloc > 0;
+    const int src = warp_lex_argmin(hv, ord_double(hv ? loc[0].k : 0.0), hv ? loc[0].tie : 0u);
+    const TopLane w = top_shfl(loc[0], src);
+    if (lane == i) x = w;
     if (lane == src) {
-      int G2, t2o, freed;
-      if (bidx < 0) {
-        G2 = A.bi_G2[ba];
-        t2o = t;
-        freed = A.G[ba] - G2;
-      } else {
-        G2 = E.G2[bidx];
-        t2o = E.t2[bidx] | 0x100;
-        freed = A.G[ba];
+      lk = loc[0].k;
+      lt = loc[0].tie;
+#pragma unroll
+      for (int q = 0; q < kL - 1; ++q) loc[q] = loc[q + 1];
+      --nloc;
+      --left;
+      if (nloc == 0 && left > 0) fill();
+    }
+  }
+  cnt = want;
+  all = total <= want;
+}
+
+// Warp t: the greedy victim sequence of GPU type t from the current state (the
+// §N6 ScaleResource move loop run for d moves without the G_o stop; an option
+// on type t later uses the shortest prefix that frees G_o), its accumulated
+// losses and the thresholds.  Per move: the argmin of (key, priority, option)
+// over the unmoved type-t jobs' same-type moves (i) -- the first unmoved entry
+// of the sorted top list -- and their other-type moves (ii) under free' -- a
+// warp argmin over the lanes' best evaluated ones -- with key = loss / freed.
+__device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView &A, int t) {
+  const int lane = threadIdx.x & 31, TT = R.T;
+  const long long c0 = clock64();
+  SeqTab &S = sh.sq[t];
+  int32_t *f2 = S.f2;
+  if (lane < TT) f2[lane] = sh.fr[lane];
+  if (lane < kRT) S.dfr[0][lane] = 0;
+  // a job has an other-type move iff on some other type u its smallest option
+  // fits: byte_u(gminb) < lim_u = log2(free_u) + 1 (0 for u = t or free_u = 0)
+  uint32_t lim_lo = 0, lim_hi = 0;
+  if (!(R.policy & 2)) {
+    const int f = lane < TT ? sh.fr[lane] : 0;
+    const uint32_t l = (lane == t || f <= 0) ? 0u : (uint32_t)(ilog2_pow2((uint32_t)f) + 1);
+    const uint32_t sl = lane < 4 ? l << (8 * lane) : 0u, sh_ = lane >= 4 && lane < 8 ? l << (8 * (lane - 4)) : 0u;
+    lim_lo = __reduce_or_sync(0xffffffffu, sl);
+    lim_hi = __reduce_or_sync(0xffffffffu, sh_);
+  }
+  // ---- (1) the top list: drop entries whose record changed or left the type
+  int cnt = S.tcnt;
+  bool all = S.tall != 0;
+  TopLane x{S.tk[lane], S.tt[lane], S.ta[lane], S.tp[lane]};
+  {
+    bool ok = lane < cnt;
+    if (ok) ok = A.t[x.a] == t && A.bi[x.a] != -2;
+    const uint32_t m = __ballot_sync(0xffffffffu, ok);
+    if (m != (cnt >= 32 ? 0xffffffffu : (1u << cnt) - 1)) {
+      const int nc = __popc(m);
+      const int src = lane < nc ? (int)__fns(m, 0, lane + 1) : 0;
+      x = top_shfl(x, src);
+      cnt = nc;
+    }
+  }
+  // ---- (2) refresh the stale same-type caches of the type's changed records
+  // (admitted or moved since the last recompute) and insert them
+  int nd = 0, n_ref = 0;
+  bool refill = false;
+  {
+    int32_t *qd = S.qd;
+    const int d0 = sh.dmark, d1 = sh.n_adm, nv = sh.n_vic;
+    for (int k0 = 0; k0 < (d1 - d0) + nv; k0 += 32) {
+      const int k = k0 + lane;
+      int a = -1;
+      if (k < d1 - d0) a = d0 + k;
+      else if (k < d1 - d0 + nv) a = sh.vic[k - (d1 - d0)];
+      const bool mine = a >= 0 && A.t[a] == t && A.bi[a] == -2;
+      const uint32_t mm = __ballot_sync(0xffffffffu, mine);
+      if (mine && nd + __popc(mm & ((1u << lane) - 1)) < kQ) qd[nd + __popc(mm & ((1u << lane) - 1))] = a;
+      nd += __popc(mm);
+      if (mine) refresh_i(R, A, a);  // lanes in parallel
+    }
+    __syncwarp();
+    n_ref = nd;
+    if (nd > 8 || nd > kQ) {
+      refill = true;
+    } else {
+      for (int i = 0; i < nd; ++i) {
+        const int a = qd[i], bi = A.bi[a];
+        if (bi < 0) continue;
+        const TopLane c{A.bk[a], ((uint32_t)A.pos[a] << 8) | (bi & 0xff), a, bi | (t << 16)};
+        top_insert(x, cnt, all, c);
       }
-      sh.g_key[par][wid] = bk;
-      sh.g_tie[par][wid] = tie;
-      sh.g_a[par][wid] = ba;
-      sh.g_idx[par][wid] = bidx;
-      sh.g_G2[par][wid] = G2;
-      sh.g_t2o[par][wid] = t2o;
-      sh.g_freed[par][wid] = freed;
     }
-    group_bar(1 + t, gn);
-    // every warp: the group's winner (lanes < gw hold the per-warp winners)
-    const int w = w0 + lane;
-    const bool in = lane < gw && sh.g_a[par][w] >= 0;
-    const int wl = warp_lex_argmin(in, ord_double(in ? sh.g_key[par][w] : 0.0),
-                                   in ? sh.g_tie[par][w] : 0u);
-    if (wl < 0) break;
-    const int ws = w0 + wl;
-    const int ca = sh.g_a[par][ws], t2o = sh.g_t2o[par][ws], G2 = sh.g_G2[par][ws];
-    const int t2 = t2o & 0xff, other = t2o >> 8;
-    if (lane < TT) {
-      int f = f2[lane];
-      if (lane == t) f += sh.g_freed[par][ws];
-      if (lane == t2 && other) f -= G2;
-      f2[lane] = f;
-      if (gwid == 0) sh.frs[t][m + 1][lane] = f;
+  }
+  if (refill || (!all && cnt < R.depth)) {
+    top_refill(sh, A, t, x, cnt, all);
+    if (lane == 0) atomicAdd(&sh.cnt[5], 1);
+  }
+  const long long ca = clock64();
+  // ---- (3) other-type moves: the type's jobs with an option on another type
+  // that fits, evaluated in parallel passes; each lane keeps its two best
+  int32_t *ql = S.ql;
+  const int n_t = sh.tn[t];
+  const int32_t *tl = A.tl + sh.toff[t];
+  int nl = 0, n_ii = 0;
+  Cand b1, b2;
+  b1.have = b2.have = false;
+  bool b2_known = true;
+  bool own_tl = false;  // more than kQ listed jobs: lane owns tl positions = lane mod 32
+  if (lim_lo | lim_hi) {
+    for (int k0 = 0; k0 < n_t; k0 += 32) {
+      const int k = k0 + lane;
+      int a = -1;
+      bool listed = false;
+      if (k < n_t) {
+        a = tl[k];
+        const uint64_t gb = A.gmb[a];
+        listed = (__vcmpltu4((uint32_t)gb, lim_lo) | __vcmpltu4((uint32_t)(gb >> 32), lim_hi)) != 0;
+        if (!listed) A.ei[a] = -1;
+      }
+      const uint32_t ml = __ballot_sync(0xffffffffu, listed);
+      const int slot = nl + __popc(ml & ((1u << lane) - 1));
+      if (listed && slot < kQ) ql[slot] = a;
+      nl += __popc(ml);
+      if (listed && slot >= kQ) {  // queue full: evaluate this one in place
+        compute_ii(R, A, a, f2);
+      }
     }
-    if (lane == 0) mv[m] = ca;
-    rescan = ba1 == ca;  // this thread's (i) candidate was moved
-    if (gwid == 0 && lane == 0) {  // record move m
-      const int idx = sh.g_idx[par][ws];
-      const double s2 = idx < 0 ? A.bi_s[ca] : E.s2[idx];
-      sh.mv_a[t][m] = ca;
-      sh.mv_opt[t][m] = (int)(sh.g_tie[par][ws] & 0xff);
-      sh.mv_G[t][m] = G2;
-      sh.mv_t[t][m] = t2;
-      sh.mv_T[t][m] = idx < 0 ? A.bi_T[ca] : E.T2[idx];
-      sh.mv_sc[t][m] = s2;
-      sh.cum[t][m + 1] = __dadd_rn(sh.cum[t][m], A.sc[ca] - s2);
-      sh.len[t] = m + 1;
+    __syncwarp();
+    n_ii = nl;
+    own_tl = nl > kQ;
+    const int nq = min(nl, kQ);
+    for (int i = lane; i < nq; i += 32) compute_ii(R, A, ql[i], f2);
+    __syncwarp();
+    if (!own_tl) {
+      for (int i = lane; i < nq; i += 32) {
+        const int a = ql[i];
+        top2_take(b1, b2, ii_cand(A, a, A.ei[a]));
+      }
+    } else {
+      for (int k = lane; k < n_t; k += 32) {
+        const int a = tl[k];
+        top2_take(b1, b2, ii_cand(A, a, A.ei[a]));
+      }
+    }
+  } else {
+    for (int k = lane; k < n_t; k += 32) A.ei[tl[k]] = -1;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    atomicAdd(&sh.cnt[0], n_ref);
+    atomicAdd(&sh.cnt[1], n_ii);
+    atomicAdd(&sh.cnt[4], n_t);
+  }
+  const long long c1 = clock64();
+  // ---- (4) the moves
+  bool imov = false;  // this lane's top-list entry was moved
+  int m = 0, n_rescan = 0;
+  for (; m < R.depth; ++m) {
+    const uint32_t im = __ballot_sync(0xffffffffu, lane < cnt && !imov);
+    const int h = im ? __ffs(im) - 1 : 0;
+    const double hk = __shfl_sync(0xffffffffu, x.k, h);
+    const uint32_t ht = __shfl_sync(0xffffffffu, x.tie, h);
+    const int src = warp_lex_argmin(b1.have, ord_double(b1.have ? b1.key : 0.0), b1.tie);
+    const double sk = __shfl_sync(0xffffffffu, b1.key, max(src, 0));
+    const uint32_t st = __shfl_sync(0xffffffffu, b1.tie, max(src, 0));
+    int wa, wpk;
+    bool wii;
+    if (im && (src < 0 || key_less(hk, ht, sk, st))) {
+      wa = __shfl_sync(0xffffffffu, x.a, h);
+      wpk = __shfl_sync(0xffffffffu, x.pk, h);
+      wii = false;
+    } else if (src >= 0) {
+      wa = __shfl_sync(0xffffffffu, b1.a, src);
+      wpk = __shfl_sync(0xffffffffu, b1.pk, src);
+      wii = true;
+    } else {
+      break;
+    }
+    const int Gc = A.G[wa], G2 = 1 << ((wpk >> 8) & 0xff), t2 = (wpk >> 16) & 0xff;
+    const int freed = wii ? Gc : Gc - G2;
+    if (lane == t) f2[t] += freed;
+    if (wii && lane == t2) f2[t2] -= G2;
+    if (lane == 0) {
+      S.mv_a[m] = wa;
+      S.mv_pk[m] = wpk;
+    }
+    __syncwarp();
+    if (lane < TT) S.dfr[m + 1][lane] = f2[lane] - sh.fr[lane];
+    if (lane < cnt && x.a == wa) imov = true;
+    bool rs = false;
+    if (b2.have && b2.a == wa) {  // the moved job's other-type entry leaves the lane's pair
+      b2.have = false;
+      b2_known = false;
+    }
+    if (b1.have && b1.a == wa) {  // promote the second best
+      b1 = b2;
+      b2.have = false;
+      rs = !b2_known;
+      b2_known = false;
+    }
+    if (wii) {  // an other-type move only shrinks free' of type t2
+      if (b1.have && !ii_fits(b1.pk, f2)) rs = true;
+      if (b2.have && !ii_fits(b2.pk, f2)) {
+        b2.have = false;
+        b2_known = false;
+      }
+    }
+    if (rs) {  // this lane's own jobs again (moved ones excluded, lost options re-evaluated)
+      ++n_rescan;
+      b1.have = b2.have = false;
+      b2_known = true;
+      const int n_own = own_tl ? n_t : min(nl, kQ);
+      for (int i = lane; i < n_own; i += 32) {
+        const int a = own_tl ? tl[i] : ql[i];
+        bool moved = false;
+        for (int q = 0; q <= m; ++q) moved |= S.mv_a[q] == a;
+        if (moved) continue;
+        int ei = A.ei[a];
+        if (ei >= 0 && !ii_fits(ei, f2)) ei = compute_ii(R, A, a, f2);
+        top2_take(b1, b2, ii_cand(A, a, ei));
+      }
     }
     __syncwarp();
   }
+  n_rescan = __reduce_add_sync(0xffffffffu, n_rescan);
+  if (lane == 0) atomicAdd(&sh.cnt[3], n_rescan);
+  // the top list persists (the moves were speculative)
+  S.tk[lane] = x.k;
+  S.tt[lane] = x.tie;
+  S.ta[lane] = x.a;
+  S.tp[lane] = x.pk;
+  if (lane == 0) {
+    S.tcnt = cnt;
+    S.tall = all;
+  }
+  const long long c2 = clock64();
+  // ---- (5) accumulated losses in move order (fp64, sequential as in the oracle)
+  double loss = 0.0;
+  if (lane < m) {
+    const int a = S.mv_a[lane], p = A.pos[a], po = A.po[a];
+    int lg, t3;
+    double sc, s2;
+    opt_get(R, A, po, p, A.cur[a], lg, t3, sc);
+    opt_get(R, A, po, p, S.mv_pk[lane] & 0xff, lg, t3, s2);
+    loss = __dsub_rn(sc, s2);
+  }
+  double acc = 0.0;
+  for (int q = 0; q < m; ++q) {
+    acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, loss, q));
+    if (lane == 0) S.cum[q + 1] = acc;
+  }
+  if (lane == 0) {
+    S.cum[0] = 0.0;
+    S.len = m;
+  }
+  __syncwarp();
+  // thresholds: lane lg -> the shortest prefix with 2^lg <= free[t] + freed
+  if (lane < kLgMax) {
+    const int G = 1 << lane;
+    double th = __longlong_as_double(0x7ff0000000000000ll);  // +inf: never succeeds
+    int mm = -1;
+    for (int q = 0; q <= m; ++q)
+      if (G <= sh.fr[t] + S.dfr[q][t]) {
+        th = S.cum[q];
+        mm = q;
+        break;
+      }
+    S.thr[lane] = th;
+    S.thm[lane] = (int8_t)mm;
+  }
+  if (lane == 0) {
+    const long long c3 = clock64();
+    atomicAdd((unsigned long long *)&sh.prof[3], (unsigned long long)(c1 - c0));
+    atomicAdd((unsigned long long *)&sh.prof[4], (unsigned long long)(c2 - c1));
+    atomicAdd((unsigned long long *)&sh.prof[5], (unsigned long long)(c3 - c2));
+    atomicAdd((unsigned long long *)&sh.prof2[0], (unsigned long long)(ca - c0));
+  }
 }
 
-// All threads: the victim sequences of every stale GPU type from the current
-// state.  (1) refresh the stale same-type caches (one warp per job); (2) list
-// the jobs that may have an other-type move (smallest option G <= the largest
-// free count of another type -- free' of the other types only decreases along
-// a sequence, so this superset holds for every move); (3) their best
-// other-type move under the current free counts (one warp per job); (4) one
-// warp per stale type runs its d moves from shared-memory caches only.
-__device__ void compute_all_seqs(RoundShared &sh, const RoundBuf &R, const AdmView &A,
-                                 int32_t *list, const EView &Es) {
-  const int tid = threadIdx.x, wid = tid >> 5;
-  const int TT = R.T, n_adm = sh.n_adm;
-  if (tid < TT) {
-    const int c = !sh.seq_ok[tid];
-    sh.comp[tid] = c;
-    if (c) {
-      sh.len[tid] = 0;
-      sh.cum[tid][0] = 0.0;
-      sh.gmin_type[tid] = INT32_MAX;
-      int fm = -1;
-      for (int q = 0; q < TT; ++q)
-        if (q != tid) fm = max(fm, sh.fr[q]);
-      sh.fmax_other[tid] = (R.policy & 2) ? -1 : fm;  // NH: no other-type victim move
+// After a commit (warp 0, lane u checks type u): drop the sequences the commit
+// can have changed -- the types whose job set or a job's option changed, and
+// the types one of whose jobs has an option on a type whose free count changed
+// and that fits under the old or the new count (that changes its other-type
+// moves).
+__device__ __forceinline__ void invalidate(RoundShared &sh, int TT, uint32_t changed, int policy) {
+  const int u = threadIdx.x & 31;
+  bool bad = false;
+  if (u < TT && !((sh.stale >> u) & 1)) {
+    bad = (changed >> u) & 1;
+    if (!(policy & 2)) {
+      const uint64_t gq = sh.sq[u].gq;
+      for (int q = 0; q < TT && !bad; ++q) {
+        if (q == u || sh.old_fr[q] == sh.fr[q]) continue;
+        const int g = byte_of(gq, q);
+        bad = g != 0xff && (1 << g) <= max(sh.old_fr[q], sh.fr[q]);
+      }
     }
   }
-  if (tid < TT * TT && !sh.seq_ok[tid / TT]) {
-    sh.frs[tid / TT][0][tid % TT] = sh.fr[tid % TT];
-    sh.fr_base[tid / TT][tid % TT] = sh.fr[tid % TT];
-  }
-  if (tid == 0) {
-    sh.n_dirty = 0;
-    sh.p_used = 0;
-  }
-  long long t0 = clock64();
-  __syncthreads();
-  // (1) stale same-type caches -> list -> one warp per job
-  for (int a = tid; a < n_adm; a += kRoundThreads)
-    if (A.bi_opt[a] == -2) list[atomicAdd(&sh.n_dirty, 1)] = a;
-  CRIUS_CHECK(n_adm <= R.J);
-  __syncthreads();
-  for (int k = wid; k < sh.n_dirty; k += kRoundWarps) refresh_victim_cache(R, A, list[k]);
-  if (tid == 0) sh.n_list = 0;
-  __syncthreads();
-  if (tid == 0) {
-    const long long t1 = clock64();
-    sh.prof[0] += t1 - t0;
-    sh.prof[4] += sh.n_dirty;
-    t0 = t1;
-  }
-  // (2) gmin per type; listed jobs
-  for (int a = tid; a < n_adm; a += kRoundThreads) {
-    const int myt = A.t[a];
-    if (!sh.comp[myt]) continue;
-    const int g = A.gmin[a];
-    atomicMin(&sh.gmin_type[myt], g);
-    if (g <= sh.fmax_other[myt]) list[atomicAdd(&sh.n_list, 1)] = a;
-  }
-  __syncthreads();
-  const int nE = sh.n_list;
-  const EView E = nE <= kECap ? Es : R.eg;
-  if (tid == 0) {
-    const long long t1 = clock64();
-    sh.prof[1] += t1 - t0;
-    sh.prof[5] += nE;
-    t0 = t1;
-  }
-  // (3) best other-type move of each listed job under the current free counts
-  OptPool pl{sh.p_T2, sh.p_s2, sh.p_G2, sh.p_ti, sh.e_po, sh.e_pn, &sh.p_used};
-  const OptPool *pool = nE <= kECap ? &pl : nullptr;
-  for (int k = wid; k < nE; k += kRoundWarps) other_type_best_warp(R, A, list[k], sh.fr, E, k, pool);
-  __syncthreads();
-  if (tid == 0) {
-    const long long t1 = clock64();
-    sh.prof[2] += t1 - t0;
-    t0 = t1;
-  }
-  // (4) one warp per stale type
-  {
-#ifndef CRIUS_SEQ_WARPS
-#define CRIUS_SEQ_WARPS 32
-#endif
-    const int gw = min(CRIUS_SEQ_WARPS, kRoundWarps / TT), t = wid / gw;  // warps per type
-    if (t < TT && sh.comp[t]) type_sequence(sh, R, A, list, nE, E, pool, t, gw);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    const long long t1 = clock64();
-    sh.prof[3] += t1 - t0;
-  }
-  if (tid < TT && sh.comp[tid]) sh.seq_ok[tid] = 1;
-  __syncthreads();
-}
-
-// Warp 0 after a commit (lane t checks type t): drop the sequences the commit
-// can have changed.  sh.changed = types whose job set or a job's option changed;
-// sh.old_fr = free counts before the commit.
-__device__ __forceinline__ void invalidate_seqs(RoundShared &sh, int TT) {
-  const int t = threadIdx.x & 31;
-  if (t >= TT || !sh.seq_ok[t]) return;
-  bool bad = (sh.changed >> t) & 1;
-  for (int q = 0; q < TT && !bad; ++q)
-    if (q != t && sh.old_fr[q] != sh.fr[q] && sh.gmin_type[t] <= max(sh.old_fr[q], sh.fr[q]))
-      bad = true;
-  if (bad) {
-    sh.seq_ok[t] = 0;
-    atomicAdd(&sh.n_invalid, 1);
+  const uint32_t m = __ballot_sync(0xffffffffu, bad);
+  if (u == 0) {
+    sh.stale |= m;
+    sh.cnt[2] += __popc(m);
   }
 }
 
@@ -691,7 +802,7 @@ __device__ __forceinline__ int warp_best_option(const OptRec *o, int nopt, Pred 
   int best = -1;
   OptRec bo{kInf, 0, 0};
   for (int i = lane; i < nopt; i += 32) {
-    const OptRec x = o[i];
+    const OptRec x = ldg_opt(o + i);
     if (pred(i, x) && (best < 0 || kappa_less(x, bo))) {
       best = i;
       bo = x;
@@ -701,297 +812,483 @@ __device__ __forceinline__ int warp_best_option(const OptRec *o, int nopt, Pred 
   return src < 0 ? -1 : __shfl_sync(0xffffffffu, best, src);
 }
 
-// (Re)point admitted record a at option `opt` (G, t, T, score) of job `pos`.
-__device__ __forceinline__ void adm_set(const AdmView &A, const RoundBuf &R, int a, int pos, int opt,
-                                        int G, int t, int64_t T, double sc) {
-  A.pos[a] = pos;
-  A.cur[a] = opt;
+__device__ __forceinline__ void gq_join(RoundShared &sh, int t, uint64_t gb) {
+  uint64_t &g = sh.sq[t].gq;
+  g = ((uint64_t)__vminu4((uint32_t)(g >> 32), (uint32_t)(gb >> 32)) << 32) |
+      __vminu4((uint32_t)g, (uint32_t)gb);
+}
+
+// Thread 0: (re)point admitted record a at option (idx, G, t).
+__device__ __forceinline__ void adm_point(RoundShared &sh, const AdmView &A, int a, int idx, int G,
+                                          int t) {
+  if (A.t[a] != t) {
+    list_remove(sh, A, a);
+    list_add(sh, A, a, t);
+    gq_join(sh, t, A.gmb[a]);
+  }
+  A.cur[a] = idx;
   A.G[a] = G;
   A.t[a] = t;
-  A.T[a] = T;
-  A.sc[a] = sc;
-  A.bi_opt[a] = -2;
-  R.cur[pos] = opt;
+  A.bi[a] = -2;
+  sh.vic[sh.n_vic++] = a;
+}
+// po: the record's pool offset (allocated by the caller), -1 = none
+__device__ __forceinline__ void adm_new(RoundShared &sh, const AdmView &A, int w, int pos, int idx,
+                                        int G, int t, int po) {
+  const int a = sh.n_adm++;
+  const uint64_t gb = sh.bs_gmb[w];
+  A.gmb[a] = gb;
+  A.tsb[a] = sh.bs_tsb[w];
+  A.nopt[a] = sh.bs_nopt[w];
+  gq_join(sh, t, gb);
+  A.po[a] = po;
+  A.pos[a] = pos;
+  A.cur[a] = idx;
+  A.G[a] = G;
+  A.t[a] = t;
+  A.bi[a] = -2;
+  A.ei[a] = -1;
+  list_add(sh, A, a, t);
 }
 
-// All threads: stage positions [w0, w0 + cap) into the shared window.
-__device__ void load_window(JobWin &W, const RoundBuf &R, int w0) {
-  const int tid = threadIdx.x;
-  const int wn = min(W.cap, R.J - w0);
-  for (int i = tid; i < wn; i += kRoundThreads) {
-    W.ref[i] = R.ref[w0 + i];
-    W.nopt[i] = R.nopt[w0 + i];
-    W.ng[i] = R.ng[w0 + i];
-    W.cand[i] = R.cand[w0 + i];
-  }
-  const int n = wn * R.maxopt;
-  const longlong2 *so = reinterpret_cast<const longlong2 *>(R.opt + (int64_t)w0 * R.maxopt);
-  longlong2 *d = reinterpret_cast<longlong2 *>(W.opt);
-  for (int i = tid; i < n; i += kRoundThreads) {
-    d[i] = so[i];
-    W.score[i] = R.score[(int64_t)w0 * R.maxopt + i];
-  }
-  W.w0 = w0;
-  W.wn = wn;
-  __syncthreads();
+__device__ __forceinline__ int res_idx(int r) { return r & 0xff; }
+__device__ __forceinline__ int res_G(int r) { return 1 << ((r >> 8) & 0x1f); }
+__device__ __forceinline__ int res_t(int r) { return (r >> 13) & 0x7; }
+__device__ __forceinline__ int res_m(int r) { return (r >> 16) & 0x1f; }
+
+// First set bit over per-warp ballot words (every lane of the calling warp
+// gets it); kRoundThreads if none.
+__device__ __forceinline__ int first_bit(const uint32_t *w) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t x = lane < kRoundWarps ? w[lane] : 0u;
+  const uint32_t b = __ballot_sync(0xffffffffu, x != 0);
+  if (!b) return kRoundThreads;
+  const int fw = __ffs(b) - 1;
+  return fw * 32 + __ffs(__shfl_sync(0xffffffffu, x, fw)) - 1;
 }
 
-// K6.  Speculative batches: warp w evaluates job pos0 + w against the current
-// state.  A job that stays pending changes nothing, so the first job of the
-// batch that is admitted (directly or through ScaleResource) is committed and
-// the next batch starts right after it -- exactly the sequential §N6 order.
-__global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, int adm_in_smem,
-                                                                   AdmView Aglob, int win_cap) {
+// Bytes of dynamic shared memory per admitted record (the AdmView fields; the
+// type lists add 4 bytes per entry, bounded per type by its GPU count).
+constexpr int kRecBytes = 4 * 8 + 9 * 4;
+constexpr int kAO = 8;  // arrival options a batch thread keeps in registers
+
+// Warp: copy the options of records [a0, a1) into the pool (two records per
+// pass, 16 lanes each).
+__device__ __forceinline__ void stage_options(const RoundBuf &R, const AdmView &A, int a0, int a1) {
+  const int lane = threadIdx.x & 31;
+  for (int a = a0 + (lane >> 4); a < a1; a += 2) {
+    const int po = A.po[a];
+    if (po < 0) continue;
+    const int p = A.pos[a], nv = A.nopt[a];
+    for (int i = lane & 15; i < nv; i += 16) {
+      const OptRec o = ldg_opt(R.opt + (int64_t)p * R.maxopt + i);
+      A.ppk[po + i] = ilog2_pow2((uint32_t)o.G) | (o.t << 8);
+      A.psc[po + i] = __ldg(R.score + (int64_t)p * R.maxopt + i);
+    }
+  }
+}
+
+// Warp: copy job `pos`'s nv options into the pool at po.
+__device__ __forceinline__ void stage_job(const RoundBuf &R, const AdmView &A, int pos, int nv, int po) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < nv; i += 32) {
+    const OptRec o = ldg_opt(R.opt + (int64_t)pos * R.maxopt + i);
+    A.ppk[po + i] = ilog2_pow2((uint32_t)o.G) | (o.t << 8);
+    A.psc[po + i] = __ldg(R.score + (int64_t)pos * R.maxopt + i);
+  }
+}
+
+__device__ __forceinline__ int pool_alloc(RoundShared &sh, int nv) {
+  if (sh.p_used + nv > sh.p_cap) return -1;
+  const int po = sh.p_used;
+  sh.p_used += nv;
+  return po;
+}
+
+// K6.
+__global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
   __shared__ RoundShared sh;
   extern __shared__ __align__(16) unsigned char dsm[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int TT = R.T;
-  // dynamic shared memory: [window][admitted records]
-  unsigned char *p = dsm;
-  JobWin W;
-  W.cap = win_cap;
-  W.opt = (OptRec *)p;
-  p += (size_t)win_cap * R.maxopt * sizeof(OptRec);
-  W.score = (double *)p;
-  p += (size_t)win_cap * R.maxopt * sizeof(double);
-  W.ref = (int64_t *)p;
-  p += (size_t)win_cap * 8;
-  W.nopt = (int32_t *)p;
-  p += (size_t)win_cap * 4;
-  W.ng = (int32_t *)p;
-  p += (size_t)win_cap * 4;
-  W.cand = (int8_t *)p;
-  p += (size_t)win_cap * 8;
-  AdmView A = Aglob;
-  if (adm_in_smem) {
-    A.T = (int64_t *)p;
-    A.bi_T = A.T + kAdmSmem;
-    A.sc = (double *)(A.bi_T + kAdmSmem);
-    A.bi_key = A.sc + kAdmSmem;
-    A.bi_s = A.bi_key + kAdmSmem;
-    A.pos = (int32_t *)(A.bi_s + kAdmSmem);
-    A.cur = A.pos + kAdmSmem;
-    A.G = A.cur + kAdmSmem;
-    A.t = A.G + kAdmSmem;
-    A.nopt = A.t + kAdmSmem;
-    A.bi_opt = A.nopt + kAdmSmem;
-    A.bi_G2 = A.bi_opt + kAdmSmem;
-    A.gmin = A.bi_G2 + kAdmSmem;
-  }
-  int32_t *list = adm_in_smem ? (int32_t *)(A.gmin + kAdmSmem) : R.list;
+  const int TT = R.T, J = R.J;
   if (tid < TT) sh.fr[tid] = R.free_io[tid];
+  if (tid < 8) {
+    sh.prof[tid] = 0;
+    sh.prof2[tid] = 0;
+    sh.cnt[tid] = 0;
+  }
   if (tid == 0) {
     sh.n_adm = 0;
-    sh.n_invalid = 0;
+    sh.stale = (1u << TT) - 1;
+    sh.dmark = 0;
+    sh.n_vic = 0;
   }
-  if (tid < kRT) sh.seq_ok[tid] = 0;
-  if (tid == 0) sh.changed = 0;
-  if (tid < 12) sh.prof[tid] = 0;
+  if (tid < kRT) {
+    sh.sq[tid].tcnt = 0;
+    sh.sq[tid].tall = 1;
+    sh.sq[tid].gq = ~0ull;
+  }
   __syncthreads();
-  long long c_start = clock64(), c_seq = 0, n_batches = 0, n_seq = 0, n_scale = 0, n_bb = 0;
-  load_window(W, R, 0);
-  // running jobs start admitted, in priority order (NEXT-4 round state)
+  long long c_start = clock64();
+
+  // ---- capacity: every admitted job holds >= 1 GPU of its type, and GPUs are
+  // conserved per type, so type u never holds more than its free count + the
+  // GPUs its running jobs hold; records <= min(J, sum over types)
+  if (tid < TT) sh.tcap[tid] = (unsigned long long)sh.fr[tid];
+  __syncthreads();
+  if (R.run_cell)
+    for (int pos = tid; pos < J; pos += kRoundThreads) {
+      const int ro = R.run_opt[pos];
+      if (ro >= 0) {
+        const OptRec x = R.opt[(int64_t)pos * R.maxopt + ro];
+        atomicAdd(&sh.tcap[x.t], (unsigned long long)x.G);
+      }
+    }
+  __syncthreads();
+  int64_t cap_sum = 0, list_sum = 0;
+  for (int u = 0; u < TT; ++u) {
+    if (sh.tcap[u] > (1ull << 30)) {  // int32 free counts along a sequence stay exact below 2^31
+      if (tid == 0) *R.err = 2;
+      return;
+    }
+    cap_sum += (int64_t)sh.tcap[u];
+  }
+  const int max_adm = (int)min(cap_sum, (int64_t)J);
+  for (int u = 0; u < TT; ++u) list_sum += min((int64_t)sh.tcap[u], (int64_t)max_adm);
+  const int64_t rec_bytes = (int64_t)max_adm * kRecBytes + list_sum * 4;
+  const bool in_smem = rec_bytes <= R.smem_bytes;
+  AdmView A = R.glob;
+  int pcap = 0;
+  if (in_smem) {
+    unsigned char *p = dsm;
+    A.bk = (double *)p;
+    A.ek = A.bk + max_adm;
+    A.gmb = (uint64_t *)(A.ek + max_adm);
+    A.tsb = A.gmb + max_adm;
+    A.pos = (int32_t *)(A.tsb + max_adm);
+    A.cur = A.pos + max_adm;
+    A.G = A.cur + max_adm;
+    A.t = A.G + max_adm;
+    A.slot = A.t + max_adm;
+    A.bi = A.slot + max_adm;
+    A.ei = A.bi + max_adm;
+    A.nopt = A.ei + max_adm;
+    A.po = A.nopt + max_adm;
+    A.tl = A.po + max_adm;
+    // the rest is the option pool: 12 bytes per option
+    const int64_t pb = (rec_bytes + 15) & ~15ll;
+    pcap = (int)max((int64_t)0, min((R.smem_bytes - pb) / 12, (int64_t)INT32_MAX / 2));
+    A.psc = (double *)(dsm + pb);
+    A.ppk = (int32_t *)(A.psc + pcap);
+  }
+  if (tid == 0) {
+    int o = 0;
+    for (int u = 0; u < TT; ++u) {
+      sh.toff[u] = o;
+      o += in_smem ? (int)min((int64_t)sh.tcap[u], (int64_t)max_adm) : J;
+      sh.tn[u] = 0;
+    }
+    sh.toff[TT] = o;
+    sh.p_used = 0;
+    sh.p_cap = pcap;
+  }
+  __syncthreads();
+
+  // ---- running jobs start admitted, in priority order (NEXT-4 round state)
   if (R.run_cell) {
-    __shared__ int32_t wsum[kRoundWarps];
     int base = 0;
-    for (int p0 = 0; p0 < R.J; p0 += kRoundThreads) {
+    for (int p0 = 0; p0 < J; p0 += kRoundThreads) {
       const int pos = p0 + tid;
-      const int ro = pos < R.J ? R.run_opt[pos] : -1;
+      const int ro = pos < J ? R.run_opt[pos] : -1;
       const unsigned b = __ballot_sync(0xffffffffu, ro >= 0);
-      if (lane == 0) wsum[wid] = __popc(b);
+      if (lane == 0) sh.wsum[wid] = __popc(b);
       __syncthreads();
       int before = base;
-      for (int w = 0; w < wid; ++w) before += wsum[w];
+      for (int w = 0; w < wid; ++w) before += sh.wsum[w];
       if (ro >= 0) {
         const int a = before + __popc(b & ((1u << lane) - 1));
         const OptRec x = R.opt[(int64_t)pos * R.maxopt + ro];
-        adm_set(A, R, a, pos, ro, x.G, x.t, x.T, R.score[(int64_t)pos * R.maxopt + ro]);
+        A.pos[a] = pos;
+        A.cur[a] = ro;
+        A.G[a] = x.G;
+        A.t[a] = x.t;
+        A.bi[a] = -2;
+        A.ei[a] = -1;
+        A.gmb[a] = R.gminb[pos];
+        A.tsb[a] = R.tsb[pos];
         A.nopt[a] = R.nopt[pos];
       }
-      for (int w = 0; w < kRoundWarps; ++w) base += wsum[w];
+      for (int w = 0; w < kRoundWarps; ++w) base += sh.wsum[w];
       __syncthreads();
     }
-    if (tid == 0) sh.n_adm = base;
+    // type lists: warp u appends its type's records (in record order)
+    if (wid < TT) {
+      int n = 0;
+      int32_t *tl = A.tl + sh.toff[wid];
+      for (int a0 = 0; a0 < base; a0 += 32) {
+        const int a = a0 + lane;
+        const bool mine = a < base && A.t[a] == wid;
+        const unsigned b = __ballot_sync(0xffffffffu, mine);
+        if (mine) {
+          const int s = n + __popc(b & ((1u << lane) - 1));
+          tl[s] = a;
+          A.slot[a] = s;
+        }
+        n += __popc(b);
+      }
+      if (lane == 0) sh.tn[wid] = n;
+      uint32_t g_lo = 0xffffffffu, g_hi = 0xffffffffu;
+      for (int k = lane; k < n; k += 32) {
+        const uint64_t gb = A.gmb[tl[k]];
+        g_lo = __vminu4(g_lo, (uint32_t)gb);
+        g_hi = __vminu4(g_hi, (uint32_t)(gb >> 32));
+      }
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1) {
+        g_lo = __vminu4(g_lo, __shfl_xor_sync(0xffffffffu, g_lo, d));
+        g_hi = __vminu4(g_hi, __shfl_xor_sync(0xffffffffu, g_hi, d));
+      }
+      if (lane == 0) sh.sq[wid].gq = ((uint64_t)g_hi << 32) | g_lo;
+    }
+    // option pool offsets in record order
+    if (tid == 0) {
+      sh.n_adm = base;
+      for (int a = 0; a < base; ++a) {
+        const int nv = A.nopt[a];
+        int po = -1;
+        if (sh.p_used + nv <= sh.p_cap) {
+          po = sh.p_used;
+          sh.p_used += nv;
+        }
+        A.po[a] = po;
+      }
+    }
+    __syncthreads();
+    for (int a0 = 2 * wid; a0 < base; a0 += 2 * kRoundWarps) stage_options(R, A, a0, min(a0 + 2, base));
     __syncthreads();
   }
+  const int n_run = sh.n_adm;
 
-  // ---- Phase A: SchedArrival in priority order
+  // ---- Phase A: SchedArrival in priority order.  A window of kRoundThreads
+  // jobs (thread = job) stays in registers while its jobs are decided: each
+  // iteration evaluates the undecided jobs [lo, kRoundThreads) against the
+  // current state and commits the first that changes it.
+  long long n_batches = 0, n_seq = 0, n_scale = 0, c_seq = 0;
   long long tb = clock64();
-  for (int pos0 = 0; pos0 < R.J;) {
-    if (pos0 + kRoundWarps > W.w0 + W.wn && W.w0 + W.wn < R.J) load_window(W, R, pos0);
-    if (tid == 0) {
-      const long long t1 = clock64();
-      sh.prof[8] += t1 - tb;
-      tb = t1;
+  for (int w0 = 0; w0 < J; w0 += kRoundThreads) {
+    const int q = w0 + tid;
+    int na = 0;
+    int apk[kAO];
+    double asc[kAO];
+    if (q < J) {
+      const int cq = __ldg(R.cand + q), nq = __ldg(R.nao + q);
+#pragma unroll
+      for (int u = 0; u < kAO; ++u)
+        if (u < R.maxopt) {
+          apk[u] = __ldg(R.ao_pk + (int64_t)u * J + q);
+          asc[u] = __ldg(R.ao_sc + (int64_t)u * J + q);
+        }
+      sh.bs_gmb[tid] = __ldg(R.gminb + q);
+      sh.bs_tsb[tid] = __ldg(R.tsb + q);
+      sh.bs_nopt[tid] = __ldg(R.nopt + q);
+      na = cq ? nq : 0;
     }
-    const int q = pos0 + wid, wq = q - W.w0;
-    CRIUS_CHECK(q >= R.J || (wq >= 0 && wq < W.wn));
-    int kind = 0, opt = -1, need = 0;
-    if (q < R.J && W.cand[wq]) {
-      const int nopt = W.nopt[wq], ngj = W.ng[wq];
-      const int best = warp_best_option(W.opt + (size_t)wq * R.maxopt, nopt,
-                                        [&](int, const OptRec &x) {
-                                          return x.G <= ngj && x.G <= sh.fr[x.t];
-                                        });
-      if (best >= 0) {
-        kind = 1;
-        opt = best;
-      } else if (R.depth >= 1) {
-        need = 1;
-      }
-    }
-    if (lane == 0) {
-      sh.res_kind[wid] = kind;
-      sh.res_opt[wid] = opt;
-      sh.need[wid] = need;
-    }
-    __syncthreads();
-    ++n_batches;
-    if (tid == 0) {
-      const long long t1 = clock64();
-      sh.prof[9] += t1 - tb;
-      tb = t1;
-    }
-    const unsigned kmask = __ballot_sync(0xffffffffu, lane < kRoundWarps && sh.res_kind[lane] != 0);
-    const int fa = kmask ? __ffs(kmask) - 1 : kRoundWarps;
-    const unsigned nmask = __ballot_sync(0xffffffffu, lane < fa && sh.need[lane]);
-    if (nmask) {
-      bool stale = false;
-      for (int q = 0; q < TT; ++q) stale |= !sh.seq_ok[q];
-      if (stale) {
-        const long long c0 = clock64();
-        compute_all_seqs(sh, R, A, list,
-                         EView{sh.e_loss, sh.e_s2, sh.e_key, sh.e_T2, sh.e_i, sh.e_G2, sh.e_t2});
-        c_seq += clock64() - c0;
-        ++n_seq;
-      }
-      if (wid < fa && need) {  // ScaleResource(q): first success in kappa order
-        const int nopt = W.nopt[wq], ngj = W.ng[wq];
-        const OptRec *o = W.opt + (size_t)wq * R.maxopt;
-        const double *so = W.score + (size_t)wq * R.maxopt;
-        int best = -1, bm = 0;
-        OptRec bo{kInf, 0, 0};
-        for (int i = lane; i < nopt; i += 32) {
-          const OptRec x = o[i];
-          if (x.G > ngj) continue;
-          const int len = sh.len[x.t];
-          int m = -1;
-          for (int mm = 0; mm <= len; ++mm)
-            if (x.G <= sh.frs[x.t][mm][x.t] - sh.fr_base[x.t][x.t] + sh.fr[x.t]) {
-              m = mm;
-              break;
-            }
-          if (m < 0 || !(so[i] > sh.cum[x.t][m])) continue;
-          if (best < 0 || kappa_less(x, bo)) {
-            best = i;
-            bo = x;
-            bm = m;
+    int lo = 0;  // jobs [0, lo) of the window are decided
+    while (lo < kRoundThreads && w0 + lo < J) {
+      // (1) direct choice: the job's first arrival option (kappa order) that fits
+      bool k1 = false, need = false;
+      int r = 0;
+      if (tid >= lo && na > 0) {
+#pragma unroll
+        for (int u = 0; u < kAO; ++u)
+          if (!k1 && u < na && res_G(apk[u]) <= sh.fr[res_t(apk[u])]) {
+            k1 = true;
+            r = apk[u];
+          }
+        for (int k = kAO; k < na && !k1; ++k) {
+          const int pk = __ldg(R.ao_pk + (int64_t)k * J + q);
+          if (res_G(pk) <= sh.fr[res_t(pk)]) {
+            k1 = true;
+            r = pk;
           }
         }
-        const int src = warp_lex_argmin(best >= 0, (uint64_t)bo.T, kappa_tie(bo));
-        best = src < 0 ? -1 : __shfl_sync(0xffffffffu, best, src);
-        bm = src < 0 ? 0 : __shfl_sync(0xffffffffu, bm, src);
-        if (lane == 0 && best >= 0) {
-          sh.res_kind[wid] = 2;
-          sh.res_opt[wid] = best;
-          sh.res_m[wid] = bm;
+        need = !k1 && R.depth >= 1;
+      }
+      sh.res[tid] = r;
+      {
+        const uint32_t b1 = __ballot_sync(0xffffffffu, k1), bn = __ballot_sync(0xffffffffu, need);
+        if (lane == 0) {
+          sh.wk1[wid] = b1;
+          sh.wnd[wid] = bn;
+          sh.wk2[wid] = 0;
         }
       }
       __syncthreads();
-    }
-    if (tid == 0) {
-      const long long t1 = clock64();
-      sh.prof[10] += t1 - tb;
-      tb = t1;
-    }
-    if (tid < 32) {
-      const unsigned fmask = __ballot_sync(0xffffffffu, lane < kRoundWarps && sh.res_kind[lane] != 0);
-      const int f = fmask ? __ffs(fmask) - 1 : kRoundWarps;
+      ++n_batches;
       if (tid == 0) {
-        int adv = kRoundWarps;
-        if (f < kRoundWarps) {
-          const int pos = pos0 + f, oi = sh.res_opt[f];
-          const OptRec x = W.opt[(size_t)(pos - W.w0) * R.maxopt + oi];
-          int32_t *old_fr = sh.old_fr;
-          for (int qq = 0; qq < TT; ++qq) old_fr[qq] = sh.fr[qq];
-          unsigned changed = 1u << 31;  // bit 31: a commit happened
-          if (sh.res_kind[f] == 2) {
-            ++n_scale;
-            const int m = sh.res_m[f], t = x.t;
-            CRIUS_CHECK(m >= 0 && m <= sh.len[t] && sh.seq_ok[t]);
-            for (int mm = 0; mm < m; ++mm) {
-              const int a = sh.mv_a[t][mm];
-              changed |= (1u << A.t[a]) | (1u << sh.mv_t[t][mm]);
-              adm_set(A, R, a, A.pos[a], sh.mv_opt[t][mm], sh.mv_G[t][mm], sh.mv_t[t][mm],
-                      sh.mv_T[t][mm], sh.mv_sc[t][mm]);
-            }
-            for (int qq = 0; qq < TT; ++qq)
-              sh.fr[qq] = sh.frs[t][m][qq] - sh.fr_base[t][qq] + old_fr[qq];
-          }
-          const int kind0 = sh.res_kind[f];
-          int w = f;
-          for (;;) {  // commit job w (admitted directly, or the first job's scale result)
-            const int wq0 = pos0 + w - W.w0, o = sh.res_opt[w];
-            CRIUS_CHECK(wq0 >= 0 && wq0 < W.wn && o >= 0 && o < W.nopt[wq0]);
-            const OptRec y = W.opt[(size_t)wq0 * R.maxopt + o];
-            sh.fr[y.t] -= y.G;
-            changed |= 1u << y.t;
-            const int na = sh.n_adm;
-        CRIUS_CHECK(na < R.J);
-            adm_set(A, R, na, pos0 + w, o, y.G, y.t, y.T, W.score[(size_t)wq0 * R.maxopt + o]);
-            A.nopt[na] = W.nopt[wq0];
-            sh.n_adm += 1;
-            adv = w + 1;
-            if (kind0 != 1) break;
-            // A direct admission only lowers one free count, so a later job's
-            // direct choice stands iff its option still fits; a job that stays
-            // pending/unschedulable without ScaleResource is unaffected.
-            bool more = false;
-            while (++w < kRoundWarps && pos0 + w < R.J) {
-              const int kw = sh.res_kind[w];
-              if (kw == 1) {
-                const OptRec z = W.opt[(size_t)(pos0 + w - W.w0) * R.maxopt + sh.res_opt[w]];
-                more = z.G <= sh.fr[z.t];
-                break;
-              }
-              if (kw == 0 && !sh.need[w]) {
-                adv = w + 1;
-                continue;
-              }
-              break;
-            }
-            if (!more) break;
-          }
-          sh.changed = changed;
-        }
-        sh.advance = adv;
+        const long long t1 = clock64();
+        sh.prof[0] += t1 - tb;
+        tb = t1;
       }
-      __syncwarp();
-      if (sh.changed) invalidate_seqs(sh, TT);
-      __syncwarp();
-      if (tid == 0) sh.changed = 0;
-    }
-    __syncthreads();
-    pos0 += sh.advance;
-    if (tid == 0) {
-      const long long t1 = clock64();
-      sh.prof[11] += t1 - tb;
-      tb = t1;
+      const int fa = first_bit(sh.wk1);
+      // any job before fa that needs ScaleResource?
+      bool nb;
+      {
+        const uint32_t x = lane < kRoundWarps ? sh.wnd[lane] : 0u;
+        const int w = lane * 32;
+        const uint32_t xm = w + 32 <= fa ? x : (w < fa ? x & ((1u << (fa - w)) - 1) : 0u);
+        nb = __ballot_sync(0xffffffffu, xm != 0) != 0;
+      }
+      if (nb) {
+        if (sh.stale) {
+          const long long c0 = clock64();
+          if (wid < TT && ((sh.stale >> wid) & 1)) type_sequence(sh, R, A, wid);
+          __syncthreads();
+          if (tid == 0) {
+            sh.stale = 0;
+            sh.dmark = sh.n_adm;  // every changed record's cache is fresh again
+            sh.n_vic = 0;
+            c_seq += clock64() - c0;
+            ++n_seq;
+          }
+        }
+        // (2) ScaleResource(q): the first option in kappa order whose trial succeeds
+        bool k2 = false;
+        if (need && tid < fa) {
+          int r2 = 0;
+#pragma unroll
+          for (int u = 0; u < kAO; ++u)
+            if (!k2 && u < na) {
+              const SeqTab &S = sh.sq[res_t(apk[u])];
+              const int lg = (apk[u] >> 8) & 0x1f;
+              if (asc[u] > S.thr[lg]) {
+                k2 = true;
+                r2 = apk[u] | ((int)S.thm[lg] << 16);
+              }
+            }
+          for (int k = kAO; k < na && !k2; ++k) {
+            const int pk = __ldg(R.ao_pk + (int64_t)k * J + q);
+            const SeqTab &S = sh.sq[res_t(pk)];
+            const int lg = (pk >> 8) & 0x1f;
+            if (__ldg(R.ao_sc + (int64_t)k * J + q) > S.thr[lg]) {
+              k2 = true;
+              r2 = pk | ((int)S.thm[lg] << 16);
+            }
+          }
+          if (k2) sh.res[tid] = r2;
+        }
+        const uint32_t b2 = __ballot_sync(0xffffffffu, k2);
+        if (lane == 0) sh.wk2[wid] = b2;
+        __syncthreads();
+        if (tid == 0) {
+          const long long t1 = clock64();
+          sh.prof[1] += t1 - tb;
+          tb = t1;
+        }
+      }
+      // (3) commit the first job f that changes the state: thread 0 updates the
+      // records and free counts while warp 1 stages job f's options in the pool
+      if (wid <= 1) {
+        const int f2n = nb ? first_bit(sh.wk2) : kRoundThreads;
+        const int f = min(fa, f2n);
+        if (wid == 1) {
+          if (lane == 0) sh.po_first = f < kRoundThreads ? pool_alloc(sh, sh.bs_nopt[f]) : -1;
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          if (f < kRoundThreads && sh.po_first >= 0) stage_job(R, A, w0 + f, sh.bs_nopt[f], sh.po_first);
+        } else {
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          const int a_new = sh.n_adm;
+          if (lane == 0) {
+            int adv = kRoundThreads;
+            if (f < kRoundThreads) {
+              for (int u = 0; u < TT; ++u) sh.old_fr[u] = sh.fr[u];
+              uint32_t changed = 0;
+              if (f2n < fa) {  // ScaleResource: apply the first m moves of the type's sequence
+                ++n_scale;
+                const int rr = sh.res[f], t = res_t(rr), m = res_m(rr);
+                SeqTab &S = sh.sq[t];
+                for (int mm = 0; mm < m; ++mm) {
+                  const int a = S.mv_a[mm], pk = S.mv_pk[mm];
+                  const int t2 = (pk >> 16) & 0xff;
+                  changed |= (1u << A.t[a]) | (1u << t2);
+                  adm_point(sh, A, a, pk & 0xff, 1 << ((pk >> 8) & 0xff), t2);
+                }
+                for (int u = 0; u < TT; ++u) sh.fr[u] += S.dfr[m][u];
+                adm_new(sh, A, f, w0 + f, res_idx(rr), res_G(rr), t, sh.po_first);
+                sh.fr[t] -= res_G(rr);
+                changed |= 1u << t;
+                adv = f + 1;
+              } else {  // direct admissions, chained while later choices provably stand
+                int w = f;
+                for (;;) {
+                  const int rr = sh.res[w], t = res_t(rr);
+                  adm_new(sh, A, w, w0 + w, res_idx(rr), res_G(rr), t,
+                          w == f ? sh.po_first : pool_alloc(sh, sh.bs_nopt[w]));
+                  sh.fr[t] -= res_G(rr);
+                  changed |= 1u << t;
+                  adv = w + 1;
+                  // A direct admission only lowers one free count, so a later job's
+                  // direct choice stands iff its option still fits; a job that stays
+                  // pending without ScaleResource is unaffected.
+                  bool more = false;
+                  while (++w < kRoundThreads && w0 + w < J) {
+                    const bool wk = (sh.wk1[w >> 5] >> (w & 31)) & 1;
+                    const bool wn = (sh.wnd[w >> 5] >> (w & 31)) & 1;
+                    if (wk) {
+                      const int r2 = sh.res[w];
+                      more = res_G(r2) <= sh.fr[res_t(r2)];
+                      break;
+                    }
+                    if (!wn) {
+                      adv = w + 1;
+                      continue;
+                    }
+                    break;
+                  }
+                  if (!more) break;
+                }
+              }
+              sh.changed = changed;
+            }
+            sh.lo = adv;
+          }
+          __syncwarp();
+          if (f < kRoundThreads) {
+            invalidate(sh, TT, sh.changed, R.policy);
+            stage_options(R, A, a_new + 1, sh.n_adm);  // the chain's later records
+          }
+        }
+      }
+      __syncthreads();
+      lo = sh.lo;
+      if (tid == 0) {
+        const long long t1 = clock64();
+        sh.prof[2] += t1 - tb;
+        tb = t1;
+      }
     }
   }
+  const long long c_phaseB = clock64();
 
   // ---- Phase B: up to d sweeps of reverse scaling over admitted jobs, in
-  // priority order (running jobs were admitted first: sort by position)
-  const long long c_phaseB = clock64();
+  // priority order.  Records [0, n_run) (running jobs) and [n_run, n_adm)
+  // (Phase A) are each in priority order: merge by binary search.
   const int n_adm = sh.n_adm;
-  int32_t *ord = list;
+  int32_t *ord = R.ord;
   for (int a = tid; a < n_adm; a += kRoundThreads) {
     const int pa = A.pos[a];
-    int r = 0;
-    for (int b = 0; b < n_adm; ++b) r += A.pos[b] < pa;
-    ord[r] = a;
+    const bool first = a < n_run;
+    int lo = first ? n_run : 0, hi = first ? n_adm : n_run;  // count of the other run with pos < pa
+    const int base = lo;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (A.pos[mid] < pa) lo = mid + 1;
+      else hi = mid;
+    }
+    ord[(first ? a : a - n_run) + (lo - base)] = a;
   }
   __syncthreads();
+  long long n_bb = 0;
   for (int sweep = 0; sweep < R.depth; ++sweep) {
     if (tid == 0) sh.any_change = 0;
     __syncthreads();
@@ -1000,38 +1297,34 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       int opt = -1;
       if (a < n_adm) {
         const int pos = A.pos[a], cv = A.cur[a], Gc = A.G[a], tc = A.t[a];
-        const int64_t Tc = A.T[a];
-        opt = warp_best_option(R.opt + (int64_t)pos * R.maxopt, A.nopt[a],
-                               [&](int i, const OptRec &x) {
-                                 const int avail = sh.fr[x.t] + (x.t == tc ? Gc : 0);
-                                 return i != cv && x.G <= avail && x.T < Tc &&
-                                        (!(R.policy & 2) || x.t == tc);  // NH keeps the type
-                               });
+        const OptRec *o = R.opt + (int64_t)pos * R.maxopt;
+        const int64_t Tc = o[cv].T;
+        opt = warp_best_option(o, R.nopt[pos], [&](int i, const OptRec &x) {
+          const int avail = sh.fr[x.t] + (x.t == tc ? Gc : 0);
+          return i != cv && x.G <= avail && x.T < Tc &&
+                 (!(R.policy & 2) || x.t == tc);  // NH keeps the type
+        });
       }
-      if (lane == 0) {
-        sh.res_opt[wid] = opt;
-        if (opt >= 0) {
-          const int pos = A.pos[a];
-          const OptRec x = R.opt[(int64_t)pos * R.maxopt + opt];
-          sh.res_G[wid] = x.G;
-          sh.res_t[wid] = x.t;
-          sh.res_T[wid] = x.T;
-          sh.res_sc[wid] = R.score[(int64_t)pos * R.maxopt + opt];
-        }
-      }
+      if (lane == 0) sh.res[wid] = opt;
       __syncthreads();
-      if (tid < 32) {
-        const unsigned fmask = __ballot_sync(0xffffffffu, lane < kRoundWarps && sh.res_opt[lane] >= 0);
-        const int f = fmask ? __ffs(fmask) - 1 : kRoundWarps;
-        if (tid == 0 && f < kRoundWarps) {
+      if (tid == 0) {
+        int f = 0;
+        while (f < kRoundWarps && sh.res[f] < 0) ++f;
+        if (f < kRoundWarps) {
           const int aa = ord[a0 + f];
+          const OptRec x = R.opt[(int64_t)A.pos[aa] * R.maxopt + sh.res[f]];
           sh.fr[A.t[aa]] += A.G[aa];
-          adm_set(A, R, aa, A.pos[aa], sh.res_opt[f], sh.res_G[f], sh.res_t[f], sh.res_T[f],
-                  sh.res_sc[f]);
-          sh.fr[A.t[aa]] -= A.G[aa];
+          if (A.t[aa] != x.t) {
+            list_remove(sh, A, aa);
+            list_add(sh, A, aa, x.t);
+          }
+          A.cur[aa] = sh.res[f];
+          A.G[aa] = x.G;
+          A.t[aa] = x.t;
+          sh.fr[x.t] -= x.G;
           sh.any_change = 1;
         }
-        if (tid == 0) sh.advance = f < kRoundWarps ? f + 1 : kRoundWarps;
+        sh.advance = f < kRoundWarps ? f + 1 : kRoundWarps;
       }
       __syncthreads();
       a0 += sh.advance;
@@ -1042,9 +1335,15 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
   const long long c_end = clock64();
 
   // ---- total score in priority order (fp64, sequential: bit-reproducible)
+  for (int k = tid; k < n_adm; k += kRoundThreads) {
+    const int a = ord[k], pos = A.pos[a];
+    R.osc[k] = R.score[(int64_t)pos * R.maxopt + A.cur[a]];
+    R.cur[pos] = A.cur[a];
+  }
+  __syncthreads();
   if (tid == 0) {
     double tot = 0.0;
-    for (int k = 0; k < n_adm; ++k) tot = __dadd_rn(tot, A.sc[ord[k]]);
+    for (int k = 0; k < n_adm; ++k) tot = __dadd_rn(tot, R.osc[k]);
     *R.total = tot;
     if (R.stats) {
       R.stats[0] = n_batches;
@@ -1055,14 +1354,26 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round_greedy(RoundBuf R, i
       R.stats[5] = n_adm;
       R.stats[6] = n_scale;
       R.stats[7] = n_bb;
-      for (int q = 0; q < 6; ++q) R.stats[8 + q] = sh.prof[q];
-      R.stats[14] = sh.n_invalid;
-      for (int q = 8; q < 12; ++q) R.stats[7 + q] = sh.prof[q];
+      R.stats[8] = sh.prof[0];
+      R.stats[9] = sh.prof[1];
+      R.stats[10] = sh.prof[2];
+      R.stats[11] = sh.cnt[0];
+      R.stats[12] = sh.cnt[1];
+      R.stats[13] = sh.cnt[2];
+      R.stats[14] = in_smem;
+      R.stats[15] = max_adm;
+      R.stats[16] = sh.prof[3];
+      R.stats[17] = sh.prof[4];
+      R.stats[18] = sh.prof[5];
+      R.stats[19] = sh.cnt[3];
+      R.stats[20] = sh.cnt[4];
+      for (int k = 0; k < 3; ++k) R.stats[21 + k] = sh.prof2[k];
+      R.stats[24] = sh.prof2[3];
     }
   }
-  __syncthreads();
   if (tid < TT) R.free_io[tid] = sh.fr[tid];
-  for (int pos = tid; pos < R.J; pos += kRoundThreads) {
+  __syncthreads();
+  for (int pos = tid; pos < J; pos += kRoundThreads) {
     const int j = R.pi[pos];
     const int c = R.cur[pos];
     const bool act = R.active ? R.active[j] != 0 : true;
