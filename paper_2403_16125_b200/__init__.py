@@ -406,7 +406,8 @@ class Crius:
                 "batch_scale_cycles", "batch_commit_cycles", "stale_caches", "other_type_evals",
                 "seq_invalidations", "records_in_smem", "records_bound", "seq_scan_cycles",
                 "seq_move_cycles", "seq_tail_cycles", "seq_rescans", "seq_entries",
-                "seq_queue_cycles", "seq_refresh_cycles", "seq_other_cycles", "seq_top2_cycles")
+                "seq_queue_cycles", "seq_refresh_cycles", "seq_other_cycles", "seq_top2_cycles",
+                "commit_serial_cycles", "commit_tail_cycles")
         return dict(zip(keys, (int(x) for x in out)))
 
     def launches(self):

@@ -1010,14 +1010,27 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   // options in the rest (an option pool; jobs that find no room read the global
   // table).  It gets the whole budget.
   cudaFuncAttributes fa{};
-  CK(cudaFuncGetAttributes(&fa, k_round));
+  CK(cudaFuncGetAttributes(&fa, k_round<true>));
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   size_t dsm = (size_t)optin - fa.sharedSizeBytes - 1024;
   if (const char *cap = getenv("CRIUS_ROUND_SMEM")) dsm = std::min<size_t>(dsm, (size_t)atoll(cap));
   R.smem_bytes = (int64_t)dsm;
-  CK(cudaFuncSetAttribute(k_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-  k_round<<<1, kRoundThreads, dsm, st>>>(R);
+  // shared-memory records when they can fit (exactly known without running jobs)
+  bool smem = true;
+  if (!run_cell) {
+    int64_t nb = 0, lists = 0;
+    for (int t = 0; t < T; ++t) nb += fr[t];
+    nb = std::min<int64_t>(nb, J);
+    for (int t = 0; t < T; ++t) lists += std::min<int64_t>(fr[t], nb);
+    smem = nb * kRecBytes + lists * 4 <= (int64_t)dsm;
+  }
+  if (smem) {
+    CK(cudaFuncSetAttribute(k_round<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    k_round<true><<<1, kRoundThreads, dsm, st>>>(R);
+  } else {
+    k_round<false><<<1, kRoundThreads, 0, st>>>(R);
+  }
   CKL();
   c->launches += 2;
   int32_t rerr = 0;
@@ -1026,6 +1039,17 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   CK(cudaMemcpyAsync(total_score, c->d_total, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&rerr, c->d_rerr, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (rerr == 3) {  // the records did not fit in shared memory: the global-memory kernel
+    CK(cudaMemsetAsync(c->d_rerr, 0, 4, st));
+    k_round<false><<<1, kRoundThreads, 0, st>>>(R);
+    CKL();
+    c->launches += 1;
+    CK(cudaMemcpyAsync(decision, c->d_decision, (size_t)J * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(free_after, c->d_free, T * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(total_score, c->d_total, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&rerr, c->d_rerr, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
   if (rerr == 1) return fail(CRIUS_EINVAL, "run_cell: a running Cell's (type, G) is not one of its job's options");
   if (rerr == 2) return fail(CRIUS_EINVAL, "free + running GPUs of a type exceed 2^30");
   return CRIUS_OK;

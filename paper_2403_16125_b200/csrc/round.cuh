@@ -241,6 +241,13 @@ __device__ __forceinline__ OptRec ldg_opt(const OptRec *p) {
   return r;
 }
 
+// Cycle stamp that the compiler keeps in program order with memory accesses.
+__device__ __forceinline__ long long tstamp() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");
+  return c;
+}
+
 __device__ __forceinline__ int byte_of(uint64_t v, int u) { return (int)((v >> (8 * u)) & 0xff); }
 
 // One victim-move sequence per GPU type and the ScaleResource thresholds.
@@ -258,6 +265,7 @@ struct SeqTab {
   int32_t f2[kRT];                  // the type warp's working free'
   uint64_t gq;  // byte u <= log2 of the smallest option G on type u over the type's jobs (a lower
                 // bound: records only join a type's bound, never leave it -- conservative)
+  uint32_t iit;  // types that the sequence's other-type moves go to
   // top list: the tcnt smallest same-type (case i) candidates of the type's
   // jobs, ascending by (key, priority, option); tall = it holds all of them
   double tk[kTop];
@@ -456,7 +464,7 @@ __device__ __forceinline__ void top_insert(TopLane &x, int &cnt, bool &all, cons
 // Warp t: refill the top list with the kTopFill smallest same-type candidates
 // of type t (every record of the type has a fresh cache).  Each lane keeps a
 // sorted run of its records' 4 smallest; the warp pops the global minimum.
-__device__ __noinline__ void top_refill(const RoundShared &sh, const AdmView &A, int t, TopLane &x,
+__device__ __forceinline__ void top_refill(const RoundShared &sh, const AdmView &A, int t, TopLane &x,
                                         int &cnt, bool &all) {
   const int lane = threadIdx.x & 31;
   const int n_t = sh.tn[t];
@@ -645,6 +653,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   }
   const long long c1 = clock64();
   // ---- (4) the moves
+  uint32_t iit = 0;   // (lane 0) types of the other-type moves
   bool imov = false;  // this lane's top-list entry was moved
   int m = 0, n_rescan = 0;
   for (; m < R.depth; ++m) {
@@ -675,6 +684,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     if (lane == 0) {
       S.mv_a[m] = wa;
       S.mv_pk[m] = wpk;
+      if (wii) iit |= 1u << t2;
     }
     __syncwarp();
     if (lane < TT) S.dfr[m + 1][lane] = f2[lane] - sh.fr[lane];
@@ -744,6 +754,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   if (lane == 0) {
     S.cum[0] = 0.0;
     S.len = m;
+    S.iit = iit;
   }
   __syncwarp();
   // thresholds: lane lg -> the shortest prefix with 2^lg <= free[t] + freed
@@ -781,10 +792,18 @@ __device__ __forceinline__ void invalidate(RoundShared &sh, int TT, uint32_t cha
     bad = (changed >> u) & 1;
     if (!(policy & 2)) {
       const uint64_t gq = sh.sq[u].gq;
+      const uint32_t iit = sh.sq[u].iit;
       for (int q = 0; q < TT && !bad; ++q) {
-        if (q == u || sh.old_fr[q] == sh.fr[q]) continue;
-        const int g = byte_of(gq, q);
-        bad = g != 0xff && (1 << g) <= max(sh.old_fr[q], sh.fr[q]);
+        const int o = sh.old_fr[q], n = sh.fr[q];
+        if (q == u || o == n) continue;
+        if (n < o) {
+          // fewer free GPUs on q only removes or worsens other-type moves to q:
+          // the argmins of a sequence that made no move to q stand
+          bad = (iit >> q) & 1;
+        } else {
+          const int g = byte_of(gq, q);
+          bad = g != 0xff && (1 << g) <= n;
+        }
       }
     }
   }
@@ -906,6 +925,11 @@ __device__ __forceinline__ int pool_alloc(RoundShared &sh, int nv) {
 }
 
 // K6.
+// kSmem: the admitted records live in shared memory (the launch fails with
+// err = 3 when the round's bound on them does not fit; the host then relaunches
+// the global-memory instantiation).  With the records' address space known at
+// compile time every record access is a plain shared-memory instruction.
+template <bool kSmem>
 __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
   __shared__ RoundShared sh;
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -956,10 +980,14 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
   const int max_adm = (int)min(cap_sum, (int64_t)J);
   for (int u = 0; u < TT; ++u) list_sum += min((int64_t)sh.tcap[u], (int64_t)max_adm);
   const int64_t rec_bytes = (int64_t)max_adm * kRecBytes + list_sum * 4;
-  const bool in_smem = rec_bytes <= R.smem_bytes;
+  constexpr bool in_smem = kSmem;
+  if (kSmem && rec_bytes > R.smem_bytes) {
+    if (tid == 0) *R.err = 3;
+    return;
+  }
   AdmView A = R.glob;
   int pcap = 0;
-  if (in_smem) {
+  if (kSmem) {
     unsigned char *p = dsm;
     A.bk = (double *)p;
     A.ek = A.bk + max_adm;
@@ -1197,65 +1225,113 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
           if (f < kRoundThreads && sh.po_first >= 0) stage_job(R, A, w0 + f, sh.bs_nopt[f], sh.po_first);
         } else {
           asm volatile("bar.sync 1, 64;" ::: "memory");
+          const long long k0 = tstamp();
           const int a_new = sh.n_adm;
-          if (lane == 0) {
+          if (f < kRoundThreads && f2n < fa) {
+            // ScaleResource (lanes in parallel): the first m moves of the type's
+            // sequence (lane mm updates victim mm), the free counts (lane u),
+            // then job f's record on its option (one field per lane)
+            const int rr = sh.res[f], t = res_t(rr), m = res_m(rr), G = res_G(rr);
+            const SeqTab &S = sh.sq[t];
+            if (lane < TT) {
+              const int o = sh.fr[lane];
+              sh.old_fr[lane] = o;
+              sh.fr[lane] = o + S.dfr[m][lane] - (lane == t ? G : 0);
+            }
+            uint32_t ch = 0;
+            bool moved_type = false;
+            if (lane < m) {
+              const int a = S.mv_a[lane], pk = S.mv_pk[lane];
+              const int t2 = (pk >> 16) & 0xff, ta = A.t[a];
+              ch = (1u << ta) | (1u << t2);
+              moved_type = ta != t2;
+              A.cur[a] = pk & 0xff;
+              A.G[a] = 1 << ((pk >> 8) & 0xff);
+              A.bi[a] = -2;
+              sh.vic[sh.n_vic + lane] = a;
+            }
+            const int an = a_new;
+            switch (lane) {
+              case 0: A.pos[an] = w0 + f; break;
+              case 1: A.cur[an] = res_idx(rr); break;
+              case 2: A.G[an] = G; break;
+              case 3: A.t[an] = t; break;
+              case 4: A.bi[an] = -2; break;
+              case 5: A.ei[an] = -1; break;
+              case 6: A.gmb[an] = sh.bs_gmb[f]; break;
+              case 7: A.tsb[an] = sh.bs_tsb[f]; break;
+              case 8: A.nopt[an] = sh.bs_nopt[f]; break;
+              case 9: A.po[an] = sh.po_first; break;
+              default: break;
+            }
+            const uint32_t cm = __reduce_or_sync(0xffffffffu, ch) | (1u << t);
+            const uint32_t mt = __ballot_sync(0xffffffffu, moved_type);
+            __syncwarp();
+            if (lane == 0) {
+              ++n_scale;
+              // victims that changed type move between the type lists
+              for (uint32_t b = mt; b; b &= b - 1) {
+                const int mm = __ffs(b) - 1;
+                const int a = S.mv_a[mm], t2 = (S.mv_pk[mm] >> 16) & 0xff;
+                list_remove(sh, A, a);
+                A.t[a] = t2;
+                list_add(sh, A, a, t2);
+                gq_join(sh, t2, A.gmb[a]);
+              }
+              sh.n_vic += m;
+              sh.n_adm = an + 1;
+              list_add(sh, A, an, t);
+              gq_join(sh, t, sh.bs_gmb[f]);
+              sh.changed = cm;
+              sh.lo = f + 1;
+            }
+          } else if (lane == 0) {
             int adv = kRoundThreads;
-            if (f < kRoundThreads) {
+            if (f < kRoundThreads) {  // direct admissions, chained while later choices provably stand
               for (int u = 0; u < TT; ++u) sh.old_fr[u] = sh.fr[u];
               uint32_t changed = 0;
-              if (f2n < fa) {  // ScaleResource: apply the first m moves of the type's sequence
-                ++n_scale;
-                const int rr = sh.res[f], t = res_t(rr), m = res_m(rr);
-                SeqTab &S = sh.sq[t];
-                for (int mm = 0; mm < m; ++mm) {
-                  const int a = S.mv_a[mm], pk = S.mv_pk[mm];
-                  const int t2 = (pk >> 16) & 0xff;
-                  changed |= (1u << A.t[a]) | (1u << t2);
-                  adm_point(sh, A, a, pk & 0xff, 1 << ((pk >> 8) & 0xff), t2);
-                }
-                for (int u = 0; u < TT; ++u) sh.fr[u] += S.dfr[m][u];
-                adm_new(sh, A, f, w0 + f, res_idx(rr), res_G(rr), t, sh.po_first);
+              int w = f;
+              for (;;) {
+                const int rr = sh.res[w], t = res_t(rr);
+                adm_new(sh, A, w, w0 + w, res_idx(rr), res_G(rr), t,
+                        w == f ? sh.po_first : pool_alloc(sh, sh.bs_nopt[w]));
                 sh.fr[t] -= res_G(rr);
                 changed |= 1u << t;
-                adv = f + 1;
-              } else {  // direct admissions, chained while later choices provably stand
-                int w = f;
-                for (;;) {
-                  const int rr = sh.res[w], t = res_t(rr);
-                  adm_new(sh, A, w, w0 + w, res_idx(rr), res_G(rr), t,
-                          w == f ? sh.po_first : pool_alloc(sh, sh.bs_nopt[w]));
-                  sh.fr[t] -= res_G(rr);
-                  changed |= 1u << t;
-                  adv = w + 1;
-                  // A direct admission only lowers one free count, so a later job's
-                  // direct choice stands iff its option still fits; a job that stays
-                  // pending without ScaleResource is unaffected.
-                  bool more = false;
-                  while (++w < kRoundThreads && w0 + w < J) {
-                    const bool wk = (sh.wk1[w >> 5] >> (w & 31)) & 1;
-                    const bool wn = (sh.wnd[w >> 5] >> (w & 31)) & 1;
-                    if (wk) {
-                      const int r2 = sh.res[w];
-                      more = res_G(r2) <= sh.fr[res_t(r2)];
-                      break;
-                    }
-                    if (!wn) {
-                      adv = w + 1;
-                      continue;
-                    }
+                adv = w + 1;
+                // A direct admission only lowers one free count, so a later job's
+                // direct choice stands iff its option still fits; a job that stays
+                // pending without ScaleResource is unaffected.
+                bool more = false;
+                while (++w < kRoundThreads && w0 + w < J) {
+                  const bool wk = (sh.wk1[w >> 5] >> (w & 31)) & 1;
+                  const bool wn = (sh.wnd[w >> 5] >> (w & 31)) & 1;
+                  if (wk) {
+                    const int r2 = sh.res[w];
+                    more = res_G(r2) <= sh.fr[res_t(r2)];
                     break;
                   }
-                  if (!more) break;
+                  if (!wn) {
+                    adv = w + 1;
+                    continue;
+                  }
+                  break;
                 }
+                if (!more) break;
               }
               sh.changed = changed;
             }
             sh.lo = adv;
           }
           __syncwarp();
+          const long long k1 = tstamp();
           if (f < kRoundThreads) {
             invalidate(sh, TT, sh.changed, R.policy);
             stage_options(R, A, a_new + 1, sh.n_adm);  // the chain's later records
+          }
+          __syncwarp();
+          if (lane == 0) {
+            sh.prof[6] += k1 - k0;
+            sh.prof[7] += tstamp() - k1;
           }
         }
       }
@@ -1362,6 +1438,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       R.stats[13] = sh.cnt[2];
       R.stats[14] = in_smem;
       R.stats[15] = max_adm;
+      R.stats[26] = sh.prof[6];
+      R.stats[27] = sh.prof[7];
       R.stats[16] = sh.prof[3];
       R.stats[17] = sh.prof[4];
       R.stats[18] = sh.prof[5];
