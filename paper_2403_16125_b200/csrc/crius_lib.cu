@@ -129,7 +129,7 @@ void free_all(crius_ctx *c) {
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
                   c->d_rng, c->d_cur, c->d_free, c->d_total, c->d_round_stats, c->d_score,
                   c->d_ao_pk, c->d_nao, c->d_rerr, c->d_ord, c->d_ao_sc, c->d_osc, c->d_gminb, c->d_tsb,
-                  c->adm_glob.bk, c->adm_glob.ek, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
+                  c->adm_glob.bk, c->adm_glob.bl, c->adm_glob.ek, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
                   c->adm_glob.t, c->adm_glob.slot, c->adm_glob.bi, c->adm_glob.ei, c->adm_glob.tl,
                   c->adm_glob.gmb, c->adm_glob.tsb, c->adm_glob.nopt, c->adm_glob.po,
                   c->d_run_opt, c->d_cand, c->d_run_cell, c->d_active};
@@ -942,6 +942,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
     CK(dalloc(&c->d_osc, J));
     // admitted records in global memory (used when they exceed shared memory)
     CK(dalloc(&c->adm_glob.bk, J));
+    CK(dalloc(&c->adm_glob.bl, J));
     CK(dalloc(&c->adm_glob.ek, J));
     CK(dalloc(&c->adm_glob.pos, J));
     CK(dalloc(&c->adm_glob.cur, J));

@@ -60,7 +60,7 @@ constexpr int kLgMax = 31;  // G <= 2^30
 // (case ii) under the sequence's current free': index | log2 G2 << 8 | t2 << 16,
 // -1 none; ek its key.  slot = position in its type's list tl.
 struct AdmView {
-  double *bk, *ek;
+  double *bk, *bl, *ek;  // bl = the cached same-type move's loss
   uint64_t *gmb, *tsb;  // the job's gminb / tsb bytes (see RoundBuf)
   int32_t *pos, *cur, *G, *t, *slot, *bi, *ei, *nopt;
   int32_t *po;  // offset of the job's options in the shared-memory pool, -1 = not staged
@@ -268,7 +268,7 @@ struct SeqTab {
   uint32_t iit;  // types that the sequence's other-type moves go to
   // top list: the tcnt smallest same-type (case i) candidates of the type's
   // jobs, ascending by (key, priority, option); tall = it holds all of them
-  double tk[kTop];
+  double tk[kTop], tlo[kTop];
   uint32_t tt[kTop];
   int32_t ta[kTop], tp[kTop];
   int32_t tcnt, tall;
@@ -339,19 +339,22 @@ __device__ __forceinline__ void refresh_i(const RoundBuf &R, const AdmView &A, i
   double sc;
   opt_get(R, A, po, p, cv, lg, t2, sc);
   int bi = -1;
-  double bk = 0.0;
+  double bk = 0.0, bl = 0.0;
 #pragma unroll 4
   for (int i2 = i0; i2 < cv; ++i2) {  // ascending: strict < keeps the lowest index on ties
     double s2;
     opt_get(R, A, po, p, i2, lg, t2, s2);
-    const double k = __ddiv_rn(__dsub_rn(sc, s2), (double)(Gc - (1 << lg)));
+    const double l = __dsub_rn(sc, s2);
+    const double k = __ddiv_rn(l, (double)(Gc - (1 << lg)));
     if (bi < 0 || k < bk) {
       bi = i2 | (lg << 8);
       bk = k;
+      bl = l;
     }
   }
   A.bi[a] = bi;
   A.bk[a] = bk;
+  A.bl[a] = bl;
 }
 
 // One lane: the job's best other-type move (case ii) under free' = f2: argmin
@@ -428,7 +431,7 @@ __device__ __forceinline__ void top2_take(Cand &b1, Cand &b2, const Cand &c) {
 
 // The type warp's top list in registers: lane i holds entry i.
 struct TopLane {
-  double k;
+  double k, l;  // key, loss
   uint32_t tie;
   int a, pk;
 };
@@ -436,6 +439,7 @@ struct TopLane {
 __device__ __forceinline__ TopLane top_shfl(const TopLane &x, int src) {
   TopLane y;
   y.k = __shfl_sync(0xffffffffu, x.k, src);
+  y.l = __shfl_sync(0xffffffffu, x.l, src);
   y.tie = __shfl_sync(0xffffffffu, x.tie, src);
   y.a = __shfl_sync(0xffffffffu, x.a, src);
   y.pk = __shfl_sync(0xffffffffu, x.pk, src);
@@ -481,7 +485,7 @@ __device__ __forceinline__ void top_refill(const RoundShared &sh, const AdmView 
     for (int k = lane; k < n_t; k += 32) {
       const int a = tl[k], bi = A.bi[a];
       if (bi < 0) continue;
-      const TopLane c{A.bk[a], ((uint32_t)A.pos[a] << 8) | (bi & 0xff), a, bi | (t << 16)};
+      const TopLane c{A.bk[a], A.bl[a], ((uint32_t)A.pos[a] << 8) | (bi & 0xff), a, bi | (t << 16)};
       if (first) ++nmine;
       else if (!key_less(lk, lt, c.k, c.tie)) continue;
       int pos = 0;
@@ -548,7 +552,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   // ---- (1) the top list: drop entries whose record changed or left the type
   int cnt = S.tcnt;
   bool all = S.tall != 0;
-  TopLane x{S.tk[lane], S.tt[lane], S.ta[lane], S.tp[lane]};
+  TopLane x{S.tk[lane], S.tlo[lane], S.tt[lane], S.ta[lane], S.tp[lane]};
   {
     bool ok = lane < cnt;
     if (ok) ok = A.t[x.a] == t && A.bi[x.a] != -2;
@@ -586,7 +590,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
       for (int i = 0; i < nd; ++i) {
         const int a = qd[i], bi = A.bi[a];
         if (bi < 0) continue;
-        const TopLane c{A.bk[a], ((uint32_t)A.pos[a] << 8) | (bi & 0xff), a, bi | (t << 16)};
+        const TopLane c{A.bk[a], A.bl[a], ((uint32_t)A.pos[a] << 8) | (bi & 0xff), a, bi | (t << 16)};
         top_insert(x, cnt, all, c);
       }
     }
@@ -656,6 +660,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   uint32_t iit = 0;   // (lane 0) types of the other-type moves
   bool imov = false;  // this lane's top-list entry was moved
   int m = 0, n_rescan = 0;
+  double cacc = 0.0;  // ((0 + loss_1) + loss_2) + ... (fp64, in move order as in the oracle)
   for (; m < R.depth; ++m) {
     const uint32_t im = __ballot_sync(0xffffffffu, lane < cnt && !imov);
     const int h = im ? __ffs(im) - 1 : 0;
@@ -666,9 +671,11 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     const uint32_t st = __shfl_sync(0xffffffffu, b1.tie, max(src, 0));
     int wa, wpk;
     bool wii;
+    double wl;
     if (im && (src < 0 || key_less(hk, ht, sk, st))) {
       wa = __shfl_sync(0xffffffffu, x.a, h);
       wpk = __shfl_sync(0xffffffffu, x.pk, h);
+      wl = __shfl_sync(0xffffffffu, x.l, h);
       wii = false;
     } else if (src >= 0) {
       wa = __shfl_sync(0xffffffffu, b1.a, src);
@@ -679,11 +686,14 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     }
     const int Gc = A.G[wa], G2 = 1 << ((wpk >> 8) & 0xff), t2 = (wpk >> 16) & 0xff;
     const int freed = wii ? Gc : Gc - G2;
+    if (wii) wl = __dmul_rn(sk, (double)Gc);  // key = loss / G_cur exactly (power of two)
+    cacc = __dadd_rn(cacc, wl);
     if (lane == t) f2[t] += freed;
     if (wii && lane == t2) f2[t2] -= G2;
     if (lane == 0) {
       S.mv_a[m] = wa;
       S.mv_pk[m] = wpk;
+      S.cum[m + 1] = cacc;
       if (wii) iit |= 1u << t2;
     }
     __syncwarp();
@@ -728,6 +738,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   if (lane == 0) atomicAdd(&sh.cnt[3], n_rescan);
   // the top list persists (the moves were speculative)
   S.tk[lane] = x.k;
+  S.tlo[lane] = x.l;
   S.tt[lane] = x.tie;
   S.ta[lane] = x.a;
   S.tp[lane] = x.pk;
@@ -736,21 +747,6 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     S.tall = all;
   }
   const long long c2 = clock64();
-  // ---- (5) accumulated losses in move order (fp64, sequential as in the oracle)
-  double loss = 0.0;
-  if (lane < m) {
-    const int a = S.mv_a[lane], p = A.pos[a], po = A.po[a];
-    int lg, t3;
-    double sc, s2;
-    opt_get(R, A, po, p, A.cur[a], lg, t3, sc);
-    opt_get(R, A, po, p, S.mv_pk[lane] & 0xff, lg, t3, s2);
-    loss = __dsub_rn(sc, s2);
-  }
-  double acc = 0.0;
-  for (int q = 0; q < m; ++q) {
-    acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, loss, q));
-    if (lane == 0) S.cum[q + 1] = acc;
-  }
   if (lane == 0) {
     S.cum[0] = 0.0;
     S.len = m;
@@ -888,7 +884,7 @@ __device__ __forceinline__ int first_bit(const uint32_t *w) {
 
 // Bytes of dynamic shared memory per admitted record (the AdmView fields; the
 // type lists add 4 bytes per entry, bounded per type by its GPU count).
-constexpr int kRecBytes = 4 * 8 + 9 * 4;
+constexpr int kRecBytes = 5 * 8 + 9 * 4;
 constexpr int kAO = 8;  // arrival options a batch thread keeps in registers
 
 // Warp: copy the options of records [a0, a1) into the pool (two records per
@@ -990,7 +986,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
   if (kSmem) {
     unsigned char *p = dsm;
     A.bk = (double *)p;
-    A.ek = A.bk + max_adm;
+    A.bl = A.bk + max_adm;
+    A.ek = A.bl + max_adm;
     A.gmb = (uint64_t *)(A.ek + max_adm);
     A.tsb = A.gmb + max_adm;
     A.pos = (int32_t *)(A.tsb + max_adm);
