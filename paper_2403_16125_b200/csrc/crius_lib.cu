@@ -10,7 +10,7 @@
 #include <string>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/crius.h"
 #include "common.cuh"
@@ -45,6 +45,14 @@ crius_status fail(crius_status s, const std::string &msg) {
   } while (0)
 
 bool pow2(int64_t x) { return x >= 1 && (x & (x - 1)) == 0; }
+
+// One NVTX range per C-ABI call (SURVEY §5 tracing): nsys / ncu --nvtx show
+// the boundary calls around their kernels; a no-op without an attached tool.
+struct AbiRange {
+  explicit AbiRange(const char *name) { nvtxRangePushA(name); }
+  ~AbiRange() { nvtxRangePop(); }
+};
+#define CRIUS_ABI_RANGE() AbiRange abi_range_(__func__)
 int ilog2_host(int64_t x) {
   int e = 0;
   while ((int64_t(1) << e) < x) ++e;
@@ -72,10 +80,9 @@ struct crius_ctx {
   int32_t *d_c = nullptr, *d_tpn = nullptr;
   int64_t *d_w = nullptr, *d_act = nullptr, *d_bnd = nullptr, *d_tpv = nullptr;
   int32_t *d_rank = nullptr, *d_pi = nullptr;
-  int64_t *d_pkeys = nullptr;     // [2J] priority sort keys (double buffer)
-  int32_t *d_pvals = nullptr;     // [2J] priority sort values
-  void *d_sort_tmp = nullptr;     // cub radix-sort scratch
-  size_t sort_tmp_bytes = 0;
+  int64_t *d_pkeys = nullptr;     // [4J] priority sort keys: (submit, id), double buffered
+  int32_t *d_pvals = nullptr;     // [2J] priority sort job indices, double buffered
+  std::vector<int64_t> h_submit, h_id;  // the (submit, id) pi was computed from
   int32_t *d_scratch = nullptr;  // [J + 8] stats
   // host copies needed later
   std::vector<int32_t> cap;
@@ -111,6 +118,10 @@ struct crius_ctx {
   // kXchHdr][2][x_cap] records; x_peer[r] = rank r's window mapped over CUDA IPC
   int32_t x_rank = -1, x_world = 0;
   int64_t x_cap = 0, x_epoch = 0;
+  int64_t x_min_cap = 0;  // smallest window capacity over the ranks (read from their headers)
+  // jobs whose per-layer rows the last load / update uploaded (estimates of
+  // units outside them would read stale rows)
+  int32_t rows_j0 = 0, rows_j1 = 0;
   bool x_open = false;
   unsigned char *x_base = nullptr;
   unsigned char *x_peer[kMaxRanks] = {};
@@ -122,7 +133,7 @@ namespace {
 void free_all(crius_ctx *c) {
   void *ptrs[] = {c->d_ng, c->d_gb, c->d_kst, c->d_L, c->d_off, c->d_submit, c->d_id, c->d_c,
                   c->d_tpn, c->d_w, c->d_act, c->d_bnd, c->d_tpv, c->d_rank, c->d_pi,
-                  c->d_pkeys, c->d_pvals, c->d_sort_tmp,
+                  c->d_pkeys, c->d_pvals,
                   c->d_scratch, c->d_tmax, c->C.job, c->C.type, c->C.G, c->C.S, c->C.nplans, c->C.plan_off,
                   c->C.unit_cell_begin, c->C.unit_plan_begin, c->C.unit_weight,
                   c->d_scan_sums[0], c->d_scan_sums[1], c->d_scan_sums[2], c->d_part,
@@ -269,43 +280,32 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
     k_profile_check<<<j1 - j0, 64, 0, st>>>(c->P, j0, BA, c->d_scratch, c->d_scratch + J);
     CKL();
   }
-  // priority order: stable radix sort by id, then by submit (A-18); only the
-  // key bits in use are sorted (non-negative keys: the sign bit never differs)
-  auto key_bits = [J](const int64_t *k) {
-    int64_t mn = 0, mx = 0;
-    for (int j = 0; j < J; ++j) {
-      mn = std::min(mn, k[j]);
-      mx = std::max(mx, k[j]);
+  // priority order pi by (submit, id) (A-18): recomputed only when they changed
+  const bool same = c->h_submit.size() == (size_t)J &&
+                    std::equal(c->h_submit.begin(), c->h_submit.end(), jb->submit_time) &&
+                    std::equal(c->h_id.begin(), c->h_id.end(), jb->job_id);
+  int n_sort = 0;
+  if (!same) {
+    c->h_submit.assign(jb->submit_time, jb->submit_time + J);
+    c->h_id.assign(jb->job_id, jb->job_id + J);
+    int64_t *sa = c->d_pkeys, *ia = c->d_pkeys + J, *sb = c->d_pkeys + 2 * (size_t)J,
+            *ib = c->d_pkeys + 3 * (size_t)J;
+    int32_t *ja = c->d_pvals, *jb2 = c->d_pvals + J;
+    k_prio_tiles<<<(J + kPrioTile - 1) / kPrioTile, 1024, 0, st>>>(c->d_submit, c->d_id, J, sa, ia, ja);
+    CKL();
+    n_sort = 2;
+    for (int W = kPrioTile; W < J; W <<= 1) {
+      k_prio_merge<<<(J + 255) / 256, 256, 0, st>>>(sa, ia, ja, J, W, sb, ib, jb2);
+      CKL();
+      std::swap(sa, sb);
+      std::swap(ia, ib);
+      std::swap(ja, jb2);
+      ++n_sort;
     }
-    if (mn < 0) return 64;
-    int b = 1;
-    while (b < 63 && (mx >> b) != 0) ++b;
-    return b;
-  };
-  const int bits_id = key_bits(jb->job_id), bits_sub = key_bits(jb->submit_time);
-  const unsigned tiles = (unsigned)((J + 255) / 256);
-  int64_t *ka = c->d_pkeys, *kb = c->d_pkeys + J;
-  int32_t *va = c->d_pvals, *vb = c->d_pvals + J;
-  for (int bits : {bits_id, bits_sub}) {  // scratch for these bit ranges (normally <= the load-time query)
-    size_t need = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, ka, kb, va, vb, J, 0, bits, st));
-    if (need > c->sort_tmp_bytes) {
-      CK(cudaFree(c->d_sort_tmp));
-      CK(cudaMalloc(&c->d_sort_tmp, need));
-      c->sort_tmp_bytes = need;
-    }
+    k_priority_scatter<<<(unsigned)((J + 255) / 256), 256, 0, st>>>(ja, J, c->d_pi, c->d_rank);
+    CKL();
   }
-  k_priority_keys_id<<<tiles, 256, 0, st>>>(c->d_id, J, ka, va);
-  CKL();
-  size_t tb = c->sort_tmp_bytes;
-  CK(cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, tb, ka, kb, va, vb, J, 0, bits_id, st));
-  k_priority_keys_submit<<<tiles, 256, 0, st>>>(c->d_submit, vb, J, ka);
-  CKL();
-  tb = c->sort_tmp_bytes;
-  CK(cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, tb, ka, kb, vb, va, J, 0, bits_sub, st));
-  k_priority_scatter<<<tiles, 256, 0, st>>>(va, J, c->d_pi, c->d_rank);
-  CKL();
-  c->launches += 5 + (j1 > j0);
+  c->launches += n_sort + (j1 > j0);
   std::vector<int32_t> stats(J + 1);
   CK(cudaMemcpyAsync(stats.data(), c->d_scratch, (J + 1) * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -329,6 +329,7 @@ int64_t crius_kernel_launches(const crius_ctx *ctx) { return ctx ? ctx->launches
 
 crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cl, const crius_jobs *jb,
                                  const crius_config *cf, int32_t device, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!out) return fail(CRIUS_EINVAL, "null out");
   *out = nullptr;
   int64_t TL = 0;
@@ -401,12 +402,8 @@ crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cl, const
   CKA(dalloc(&c->d_tpn, TL));
   CKA(dalloc(&c->d_rank, J));
   CKA(dalloc(&c->d_pi, J));
-  CKA(dalloc(&c->d_pkeys, 2 * (size_t)J));
+  CKA(dalloc(&c->d_pkeys, 4 * (size_t)J));
   CKA(dalloc(&c->d_pvals, 2 * (size_t)J));
-  CKA(cub::DeviceRadixSort::SortPairs(nullptr, c->sort_tmp_bytes, (int64_t *)nullptr,
-                                      (int64_t *)nullptr, (int32_t *)nullptr, (int32_t *)nullptr,
-                                      J, 0, 64));
-  CKA(cudaMalloc(&c->d_sort_tmp, std::max<size_t>(c->sort_tmp_bytes, 16)));
   CKA(dalloc(&c->d_scratch, J + 8));
   CKA(dalloc(&c->d_counter, 4));
   CKA(dalloc(&c->d_part, 2 * 9 + 2));
@@ -423,6 +420,8 @@ crius_status crius_load_profiles(crius_ctx **out, const crius_cluster *cl, const
   P.tpn = c->d_tpn;
   s = copy_inputs(c, cl, jb, st, 0, jb->n_jobs);
   if (s != CRIUS_OK) return cleanup(s);
+  c->rows_j0 = 0;
+  c->rows_j1 = jb->n_jobs;
   s = finish_load(c, cl, jb, cf, st, 0, jb->n_jobs);
   if (s != CRIUS_OK) return cleanup(s);
 #undef CKA
@@ -439,6 +438,7 @@ crius_status crius_update_profiles(crius_ctx *c, const crius_cluster *cl, const 
 crius_status crius_update_profiles_range(crius_ctx *c, const crius_cluster *cl,
                                          const crius_jobs *jb, int32_t job_begin,
                                          int32_t job_end, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
   if (job_begin < 0 || job_end > c->P.J || job_begin > job_end)
     return fail(CRIUS_EINVAL, "update_profiles_range: bad job range");
@@ -468,11 +468,14 @@ crius_status crius_update_profiles_range(crius_ctx *c, const crius_cluster *cl,
   s = copy_inputs(c, cl, jb, st, job_begin, job_end);
   if (s != CRIUS_OK) return s;
   c->enumerated = false;
+  c->rows_j0 = job_begin;
+  c->rows_j1 = job_end;
   return finish_load(c, cl, jb, &cf, st, job_begin, job_end);
 }
 
 crius_status crius_enumerate_cells(crius_ctx *c, int64_t *n_cells, int64_t *n_plans,
                                    int64_t *n_units, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -601,6 +604,7 @@ extern "C" {
 
 crius_status crius_partition_units(crius_ctx *c, int32_t world, int64_t *unit_begin,
                                    int64_t *cell_begin, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c || !unit_begin || !cell_begin) return fail(CRIUS_EINVAL, "null argument");
   if (!c->enumerated) return fail(CRIUS_ESTATE, "partition before enumerate");
   if (world < 1 || world > 8) return fail(CRIUS_EINVAL, "world must be 1..8");
@@ -625,7 +629,8 @@ namespace {
 
 // Shared launcher of k_estimate: amode 0 = uniform plans (§N5), 1/2 = NEXT-1
 // per-stage assembly (paper DP-only/TP-only per stage; every factorisation).
-constexpr int64_t kXchHdr = 256;  // flag bytes at the head of a window
+constexpr int64_t kXchHdr = 256;     // header bytes at the head of a window: flags int64[8], ...
+constexpr int64_t kXchCapOff = 128;  // ... and the window's capacity (int64)
 
 crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_begin,
                              int64_t unit_end, crius_cell_result *d_out, int16_t *d_splits,
@@ -634,6 +639,9 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   if (!c->enumerated) return fail(CRIUS_ESTATE, "estimate before enumerate");
   if (unit_begin < 0 || unit_end > c->n_units || unit_begin > unit_end)
     return fail(CRIUS_EINVAL, "bad unit range");
+  if (unit_begin < unit_end &&
+      (unit_begin / c->P.T < c->rows_j0 || (unit_end - 1) / c->P.T >= c->rows_j1))
+    return fail(CRIUS_EINVAL, "unit range reaches jobs whose profile rows the last update did not upload");
   if (!d_out && !exchange) return fail(CRIUS_EINVAL, "null d_out");
   CK(cudaSetDevice(c->device));
   EstArgs A{};
@@ -754,6 +762,7 @@ extern "C" {
 
 crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit_end,
                                   crius_cell_result *d_out, int16_t *d_splits, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
   return launch_estimate(c, 0, 0, unit_begin, unit_end, d_out, d_splits, nullptr, nullptr,
                          (cudaStream_t)stream);
@@ -762,6 +771,7 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
 // ---- fused exchange (SURVEY §8(e) fused-collective option) -------------------
 crius_status crius_exchange_init(crius_ctx *c, int32_t rank, int32_t world, int64_t capacity_cells,
                                  uint8_t *handle_out) {
+  CRIUS_ABI_RANGE();
   if (!c || !handle_out) return fail(CRIUS_EINVAL, "null argument");
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
     return fail(CRIUS_EINVAL, "rank/world out of range (world <= 8)");
@@ -772,6 +782,8 @@ crius_status crius_exchange_init(crius_ctx *c, int32_t rank, int32_t world, int6
   CK(cudaMalloc((void **)&c->x_base, bytes));
   CK(cudaMalloc((void **)&c->x_done, sizeof(uint32_t)));
   CK(cudaMemset(c->x_base, 0, kXchHdr));
+  // the window's capacity sits in its header (offset kXchCapOff) for the peers to check
+  CK(cudaMemcpy(c->x_base + kXchCapOff, &capacity_cells, sizeof(int64_t), cudaMemcpyHostToDevice));
   CK(cudaMemset(c->x_done, 0, sizeof(uint32_t)));
   CK(cudaDeviceSynchronize());  // flags are zero before any peer can signal
   cudaIpcMemHandle_t h;
@@ -786,6 +798,7 @@ crius_status crius_exchange_init(crius_ctx *c, int32_t rank, int32_t world, int6
 }
 
 crius_status crius_exchange_open(crius_ctx *c, const uint8_t *handles) {
+  CRIUS_ABI_RANGE();
   if (!c || !handles) return fail(CRIUS_EINVAL, "null argument");
   if (!c->x_base || c->x_open) return fail(CRIUS_ESTATE, "exchange not initialised or already open");
   CK(cudaSetDevice(c->device));
@@ -800,15 +813,24 @@ crius_status crius_exchange_open(crius_ctx *c, const uint8_t *handles) {
     CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     c->x_peer[r] = (unsigned char *)p;
   }
+  // every rank stores its records into every window: the smallest capacity bounds n_cells
+  c->x_min_cap = c->x_cap;
+  for (int r = 0; r < c->x_world; ++r) {
+    int64_t cap = 0;
+    CK(cudaMemcpy(&cap, c->x_peer[r] + kXchCapOff, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    c->x_min_cap = std::min(c->x_min_cap, cap);
+  }
   c->x_open = true;
   return CRIUS_OK;
 }
 
 crius_status crius_estimate_exchange(crius_ctx *c, int64_t unit_begin, int64_t unit_end, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
   if (!c->x_open) return fail(CRIUS_ESTATE, "exchange not open");
   if (!c->enumerated) return fail(CRIUS_ESTATE, "estimate before enumerate");
-  if (c->n_cells > c->x_cap) return fail(CRIUS_EINVAL, "more Cells than the exchange capacity");
+  if (c->n_cells > c->x_min_cap)
+    return fail(CRIUS_EINVAL, "more Cells than the smallest exchange window (over the ranks)");
   c->x_epoch += 1;
   const crius_status s = launch_estimate(c, 0, 0, unit_begin, unit_end, nullptr, nullptr, nullptr,
                                          nullptr, (cudaStream_t)stream, true);
@@ -817,6 +839,7 @@ crius_status crius_estimate_exchange(crius_ctx *c, int64_t unit_begin, int64_t u
 }
 
 crius_status crius_exchange_wait(crius_ctx *c, crius_cell_result **d_all, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c || !d_all) return fail(CRIUS_EINVAL, "null argument");
   if (!c->x_open || c->x_epoch < 1) return fail(CRIUS_ESTATE, "no exchange step to wait for");
   CK(cudaSetDevice(c->device));
@@ -829,6 +852,7 @@ crius_status crius_exchange_wait(crius_ctx *c, crius_cell_result **d_all, void *
 }
 
 crius_status crius_exchange_close(crius_ctx *c) {
+  CRIUS_ABI_RANGE();
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
   if (!c->x_base) return CRIUS_OK;
   cudaSetDevice(c->device);
@@ -849,6 +873,7 @@ crius_status crius_exchange_close(crius_ctx *c) {
 crius_status crius_estimate_assembled(crius_ctx *c, const crius_assembly *asm_cfg,
                                       int64_t unit_begin, int64_t unit_end,
                                       crius_cell_result *d_out, int8_t *d_stage_tp, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c || !asm_cfg) return fail(CRIUS_EINVAL, "null argument");
   if (asm_cfg->mode != 1 && asm_cfg->mode != 2) return fail(CRIUS_EINVAL, "assembly mode must be 1 or 2");
   if (asm_cfg->pipeline_form != 0 && asm_cfg->pipeline_form != 1)
@@ -860,6 +885,7 @@ crius_status crius_estimate_assembled(crius_ctx *c, const crius_assembly *asm_cf
 crius_status crius_estimate_paper_stages(crius_ctx *c, int64_t unit_begin, int64_t unit_end,
                                         crius_cell_result *d_out, int16_t *d_splits,
                                         int8_t *d_stage_lg, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
   return launch_estimate(c, 4, 0, unit_begin, unit_end, d_out, d_splits, d_stage_lg, nullptr,
                          (cudaStream_t)stream);
@@ -868,6 +894,7 @@ crius_status crius_estimate_paper_stages(crius_ctx *c, int64_t unit_begin, int64
 crius_status crius_tune_assembled(crius_ctx *c, int32_t pipeline_form, int64_t unit_begin,
                                   int64_t unit_end, const int8_t *d_favor,
                                   crius_cell_result *d_out, int8_t *d_stage_tp, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c || !d_favor) return fail(CRIUS_EINVAL, "null argument");
   if (pipeline_form != 0 && pipeline_form != 1)
     return fail(CRIUS_EINVAL, "pipeline_form must be 0 or 1");
@@ -878,6 +905,7 @@ crius_status crius_tune_assembled(crius_ctx *c, int32_t pipeline_form, int64_t u
 crius_status crius_compact_gathered(crius_ctx *c, const crius_cell_result *d_gathered,
                                     int64_t chunk_stride, int32_t world, const int64_t *cell_begin,
                                     crius_cell_result *d_all, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c || !d_gathered || !cell_begin || !d_all) return fail(CRIUS_EINVAL, "null argument");
   if (!c->enumerated) return fail(CRIUS_ESTATE, "compact before enumerate");
   if (world < 1 || world > 8) return fail(CRIUS_EINVAL, "world must be 1..8");
@@ -909,6 +937,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
                                         const int32_t *free_gpus, const int64_t *run_cell,
                                         const uint8_t *active, int64_t *decision,
                                         int32_t *free_after, double *total_score, void *stream) {
+  CRIUS_ABI_RANGE();
   if (!c || !d_all || !decision || !free_after || !total_score)
     return fail(CRIUS_EINVAL, "null argument");
   if (!c->enumerated) return fail(CRIUS_ESTATE, "round before enumerate");
@@ -1078,6 +1107,7 @@ crius_status crius_set_deadline_bounds(crius_ctx *c, const int64_t *t_max, void 
 }
 
 crius_status crius_round_stats(crius_ctx *c, int64_t *out16, void *stream) {
+  CRIUS_ABI_RANGE();
   int64_t *out8 = out16;
   if (!c || !out16) return fail(CRIUS_EINVAL, "null argument");
   if (!c->d_round_stats) return fail(CRIUS_ESTATE, "no round has run");

@@ -176,22 +176,93 @@ __global__ void k_unit_fill(Params P, Cells C, int64_t n_units) {
   }
 }
 
-// Round priority pi (A-18): jobs ordered by (submit, id) ascending (ids are
-// unique, so the order is total).  Two stable radix sorts (cub): by id, then
-// by submit; these kernels stage the keys and scatter the result:
+// Round priority pi (A-18): jobs ordered by (submit, id) ascending.  Ids are
+// unique, so the key order is total and no sort needs to be stable: tiles of
+// kPrioTile jobs are sorted in shared memory (bitonic), then runs of doubling
+// width are merged -- each element's output position is its rank in its own
+// run plus the number of smaller keys in the partner run (binary search).
 // pi[pos] = j and rank[j] = pos.
-__global__ void k_priority_keys_id(const int64_t *id, int32_t J, int64_t *keys, int32_t *vals) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < J) {
-    keys[j] = id[j];
-    vals[j] = j;
+constexpr int kPrioTile = 2048;  // jobs per tile (1024 threads x 2)
+
+struct PrioKey {
+  int64_t sub, id;
+  int32_t j;
+};
+
+__device__ __forceinline__ bool prio_less(int64_t s1, int64_t i1, int64_t s2, int64_t i2) {
+  return s1 < s2 || (s1 == s2 && i1 < i2);
+}
+
+__global__ void __launch_bounds__(1024) k_prio_tiles(const int64_t *__restrict__ submit,
+                                                     const int64_t *__restrict__ id, int32_t J,
+                                                     int64_t *osub, int64_t *oid, int32_t *oj) {
+  __shared__ int64_t ss[kPrioTile], si[kPrioTile];
+  __shared__ int32_t sj[kPrioTile];
+  const int base = blockIdx.x * kPrioTile;
+  for (int i = threadIdx.x; i < kPrioTile; i += blockDim.x) {
+    const int j = base + i;
+    const bool in = j < J;
+    ss[i] = in ? submit[j] : INT64_MAX;  // padding sorts last (ids break the tie)
+    si[i] = in ? id[j] : INT64_MAX;
+    sj[i] = in ? j : -1;
+  }
+  __syncthreads();
+  for (int k = 2; k <= kPrioTile; k <<= 1)
+    for (int d = k >> 1; d > 0; d >>= 1) {
+      for (int i = threadIdx.x; i < kPrioTile; i += blockDim.x) {
+        const int l = i ^ d;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const bool gt = prio_less(ss[l], si[l], ss[i], si[i]) ||
+                          (ss[l] == ss[i] && si[l] == si[i] && sj[l] < sj[i]);
+          if (gt == up) {
+            const int64_t a = ss[i], b = si[i];
+            const int32_t c = sj[i];
+            ss[i] = ss[l];
+            si[i] = si[l];
+            sj[i] = sj[l];
+            ss[l] = a;
+            si[l] = b;
+            sj[l] = c;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < kPrioTile; i += blockDim.x) {
+    const int o = base + i;
+    if (o < J) {
+      osub[o] = ss[i];
+      oid[o] = si[i];
+      oj[o] = sj[i];
+    }
   }
 }
 
-__global__ void k_priority_keys_submit(const int64_t *submit, const int32_t *by_id, int32_t J,
-                                       int64_t *keys) {
+// Merge runs of width W (sorted) pairwise into runs of width 2W.
+__global__ void k_prio_merge(const int64_t *__restrict__ isub, const int64_t *__restrict__ iid,
+                             const int32_t *__restrict__ ij, int32_t J, int32_t W, int64_t *osub,
+                             int64_t *oid, int32_t *oj) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < J) keys[i] = submit[by_id[i]];
+  if (i >= J) return;
+  const int run = i / W, p = i - run * W;
+  const int pb = (run ^ 1) * W;  // partner run [pb, pe)
+  const int pe = min(pb + W, J);
+  const int64_t s = isub[i], d = iid[i];
+  int cnt = 0;
+  if (pb < J) {  // number of partner keys below (s, d)
+    int lo = pb, hi = pe;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (prio_less(isub[mid], iid[mid], s, d)) lo = mid + 1;
+      else hi = mid;
+    }
+    cnt = lo - pb;
+  }
+  const int o = (run & ~1) * W + p + cnt;
+  osub[o] = s;
+  oid[o] = d;
+  oj[o] = ij[i];
 }
 
 __global__ void k_priority_scatter(const int32_t *order, int32_t J, int32_t *pi, int32_t *rank) {

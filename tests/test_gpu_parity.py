@@ -248,26 +248,31 @@ def test_update_profiles_and_repeat(crius, oracle_mod):
 
 
 def test_update_profiles_range(crius, oracle_mod):
-    """crius_update_profiles_range: only the rows of jobs [j0, j1) change; the
-    Cells of those jobs must match the oracle on the new values, the others the
-    oracle on the old ones (their rows were not re-copied)."""
+    """crius_update_profiles_range: only the rows of jobs [j0, j1) are re-copied,
+    so the library estimates only units of those jobs (a range reaching other
+    jobs is rejected: their rows may be stale) and those Cells match the oracle
+    on the new values."""
     pkg = crius
     a, b = W.make_config(3, seed=3), W.make_config(3, seed=3)
     b.c = (b.c * 2).astype(np.int32)
     b.bnd = b.bnd + 7
     j0, j1 = 300, 650
+    T = a.n_types
     with pkg.Crius(a) as cr:
         cr.enumerate()
         cr.update(b, j0, j1)
         n, _, _ = cr.enumerate()
         cells = {k: v.cpu().numpy() for k, v in cr.cells().items()}
-        got = pkg.decode(cr.estimate())[0][:n]
-    _, _, t_a, _, _ = oracle_run(oracle_mod, a)
+        with pytest.raises(pkg.CriusError) as e:
+            cr.estimate()
+        assert e.value.code == 2 and "did not upload" in str(e.value)
+        with pytest.raises(pkg.CriusError):
+            cr.estimate(j0 * T - 1, j1 * T)
+        inr = (cells["job"] >= j0) & (cells["job"] < j1)
+        got = pkg.decode(cr.estimate(j0 * T, j1 * T))[0][:int(inr.sum())]
     _, _, t_b, _, _ = oracle_run(oracle_mod, b)
-    inr = (cells["job"] >= j0) & (cells["job"] < j1)
     assert inr.any() and (~inr).any()
-    assert np.array_equal(got[inr], t_b[inr])
-    assert np.array_equal(got[~inr], t_a[~inr])
+    assert np.array_equal(got, t_b[inr])
     with pkg.Crius(a) as cr:
         with pytest.raises(pkg.CriusError):
             cr.update(b, 5, a.n_jobs + 1)
@@ -383,5 +388,5 @@ def test_exchange_rejects_misuse(crius):
             cr.exchange_init(0, 9)
         h = cr.exchange_init(0, 1, capacity=1)
         cr.exchange_open(h)
-        with pytest.raises(Exception, match="capacity"):
+        with pytest.raises(Exception, match="exchange window"):
             cr.estimate_exchange(0, 1)
