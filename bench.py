@@ -35,17 +35,21 @@ from paper_2403_16125_b200 import workload as W  # noqa: E402
 ALU_OPS_PER_DP_PROBE = 8      # one binary-search probe of the stage DP
 ALU_OPS_PER_STAGE_EVAL = 40   # one (plan, stage) cost evaluation
 SM_COUNT = 148
+# int32 lanes per SM that execute the estimator's integer work: the ALU and the
+# FMA pipes of the 4 SMSPs, 16 lanes each (4 x (16 + 16) = 128)
 INT_LANES_PER_SM = 128
-# k_round_greedy (one CTA, sequential by definition) has no throughput roofline;
-# its floor is its chain of CTA-wide barriers: every Phase A batch needs >= 3,
-# every victim-sequence recomputation >= 4 plus one group barrier per move,
-# every Phase B batch >= 2.  Measured __syncthreads latency at 1024 threads
-# on this B200: 76.9 cycles (profiles/r1_latency_microbench.txt).
-BARRIER_CYCLES = 76.9
+# k_round (one 256-thread CTA, sequential by definition) has no throughput
+# roofline; its structural floor is its chain of CTA-wide barriers (counted by
+# the kernel: every Phase A iteration, every sequence recomputation, every
+# ScaleResource evaluation, every Phase B batch) x the measured __syncthreads
+# latency at 256 threads on this B200: 29.1 cycles
+# (profiles/r2/latency_microbench.txt).
+BARRIER_CYCLES = 29.1
+ROUND_THREADS = 256
 
 
-def round_floor(st, depth, sm_mhz):
-    n = 3 * st["phaseA_batches"] + (4 + depth) * st["seq_recomputes"] + 2 * st["phaseB_batches"]
+def round_floor(st, sm_mhz):
+    n = st["cta_barriers"]
     return n, n * BARRIER_CYCLES / (sm_mhz * 1e3)  # barriers, ms
 
 
@@ -93,7 +97,11 @@ def config_dict(a, pr, n_cells, n_plans, world, flush):
             "parallelism": f"cell-range sharding x{world} + " + (
                 "fused P2P exchange (estimate kernel -> NVLink peer windows)"
                 if world > 1 and getattr(a, "gather", "nccl") == "p2p" else "all-gather"),
-            "l2": "flushed between steps (256 MiB write)" if flush else "not flushed"}
+            "l2": "flushed between steps (256 MiB write)" if flush else "not flushed",
+            "activation_model": "stage-input activations per sample (DESIGN R-1: 2*s*h per "
+                                "transformer block, GPipe re-materialisation), not SURVEY "
+                                "§8(d)'s 34*s*h + 5*heads*s^2; it decides which plans pass the "
+                                "memory filter (PAPER.md:390)"}
 
 
 # --------------------------------------------------------------- clocks
@@ -175,11 +183,28 @@ def algorithmic_ops(pr, cells, units):
     return probes, stage_evals, ALU_OPS_PER_DP_PROBE * probes + ALU_OPS_PER_STAGE_EVAL * stage_evals
 
 
-def unique_bytes(pr, n_cells):
-    """HBM bytes the estimate must move once: profile rows read + 16 B per Cell written."""
-    K1e = pr.k_max + 1
-    return int(pr.n_types * K1e * pr.total_layers * 4 + pr.total_layers * (8 * 5 + 4)
-               + n_cells * (4 * 5 + 8) + n_cells * 16)
+def algorithmic_bytes(pr, cells):
+    """SURVEY §8(d) algorithmic HBM bytes of one full estimate: per unit (job,
+    type) the compute planes k <= log2(max g) it needs (int32 per layer; the
+    kernel stages exactly these), per job its per-layer rows once (w, act, bnd,
+    tpv int64 + tpn int32 = 36 B per layer; the other types' units re-read them
+    from L2), per Cell its table entry (G, S int32 + plan offset int64) read and
+    its 16-byte record written."""
+    T, K1e = pr.n_types, pr.k_max + 1
+    ng = pr.ng.astype(np.int64)
+    L = pr.n_layers.astype(np.int64)
+    planes = 0
+    for t in range(T):
+        cap = int(pr.cap[t])
+        if pr.gpu_set == 1:
+            gtop = np.full_like(ng, cap)
+        else:
+            gtop = np.where(2 * ng <= cap, 2 * ng, np.where(ng <= cap, ng, ng // 2))
+        g = np.minimum(np.maximum(gtop, 1), pr.g_max)
+        k1 = np.minimum(np.floor(np.log2(g)).astype(np.int64) + 1, K1e)
+        planes += int((k1 * L * 4).sum())
+    n_cells = len(cells["job"])
+    return planes + int(L.sum()) * 36 + n_cells * (16 + 16)
 
 
 def load_peaks():
@@ -442,7 +467,8 @@ def main():
     clocks = clk.summary()
     peak_ops = SM_COUNT * INT_LANES_PER_SM * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     achieved_ops = ops * frac_units / (est_ms / 1e3)
-    hbm = unique_bytes(pr, n_cells) * frac_units / (est_ms / 1e3) / 1e9
+    alg_bytes = algorithmic_bytes(pr, cells_h) * frac_units
+    hbm = alg_bytes / (est_ms / 1e3) / 1e9
 
     # e2e through the public API: pinned host inputs -> update (H2D) -> enumerate
     # -> estimate -> round (decisions D2H), same metric
@@ -505,8 +531,31 @@ def main():
                "ms_per_step": e2e_ms}
 
     rstats = cr.round_stats()
-    n_bar, floor_ms = round_floor(rstats, pr.depth, float(clocks.get("sm_mhz") or 1965.0))
+    sm_mhz = float(clocks.get("sm_mhz") or 1965.0)
+    n_bar, floor_ms = round_floor(rstats, sm_mhz)
     round_ms = float(np.median(seg[:, 3]))
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    est_roof = {"kernel": "k_estimate", "bound": "alu", "achieved": achieved_ops / 1e12,
+                "peak": peak_ops / 1e12, "unit": "Tops/s", "frac": achieved_ops / peak_ops,
+                "traffic": committed_traffic(workload_name(a)),
+                "peak_source": f"{SM_COUNT} SMs x {INT_LANES_PER_SM} int32 lanes (ALU + FMA pipes, "
+                               f"4 SMSPs x (16 + 16)) x sm_max_mhz ({src})",
+                "ops_per_launch": ops * frac_units, "dp_probes": probes,
+                "stage_evals": stage_evals, "share": est_ms / ms_per_step,
+                "hbm": {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": hbm / hbm_peak,
+                        "algorithmic_bytes_per_launch": alg_bytes,
+                        "bytes_source": "SURVEY §8(d): the compute planes each unit needs + "
+                                        "per-layer rows once per job + 32 B per Cell"}}
+    round_roof = {"kernel": "k_round", "bound": "latency", "achieved": n_bar / (round_ms * 1e3),
+                  "peak": sm_mhz / BARRIER_CYCLES, "unit": "CTA barriers/us",
+                  "frac": floor_ms / round_ms, "traffic": None, "share": round_ms / ms_per_step,
+                  "barrier_chain": n_bar, "floor_ms": floor_ms, "achieved_ms": round_ms,
+                  "peak_source": f"{n_bar} CTA barriers (counted in the kernel) x {BARRIER_CYCLES} "
+                                 f"cycles ({ROUND_THREADS}-thread __syncthreads, measured) at sm_mhz"}
+    # the top-level roofline is the dominant kernel's; the other rides beside it
+    dominant_round = round_ms >= est_ms
+    roof = dict(round_roof if dominant_round else est_roof)
+    roof["other"] = est_roof if dominant_round else round_roof
     line = {"metric": "Cell-plan evaluations/sec", "value": value, "unit": "cell-plans/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
@@ -514,26 +563,12 @@ def main():
             "config": config_dict(a, pr, n_cells, n_plans, world, flush),
             "breakdown_ms": {"enumerate": float(np.median(seg[:, 0])), "estimate": est_ms,
                              "gather": float(np.median(seg[:, 2])),
-                             "round": float(np.median(seg[:, 3]))},
+                             "round": round_ms},
             "latency_ms": {"p10": float(np.percentile(step_ms, 10)),
                            "p50": float(np.median(step_ms)),
                            "p90": float(np.percentile(step_ms, 90))},
             "estimate_evals_per_s": n_plans * frac_units / (est_ms / 1e3),
-            "roofline": {"kernel": "k_estimate", "bound": "alu", "achieved": achieved_ops / 1e12,
-                         "peak": peak_ops / 1e12, "unit": "Tops/s",
-                         "frac": achieved_ops / peak_ops,
-                         "traffic": committed_traffic(workload_name(a)),
-                         "peak_source": f"{SM_COUNT} SMs x {INT_LANES_PER_SM} int lanes x "
-                                        f"sm_max_mhz ({src})",
-                         "ops_per_launch": ops * frac_units, "dp_probes": probes,
-                         "stage_evals": stage_evals,
-                         "hbm_gbs": hbm, "hbm_frac": hbm / float(peaks.get("hbm_gbs", 6650.0)),
-                         "dominant": {"kernel": "k_round_greedy", "share": round_ms / ms_per_step,
-                                      "bound": "latency (one CTA: the round is sequential)",
-                                      "barrier_chain": n_bar, "floor_ms": floor_ms,
-                                      "achieved_ms": round_ms, "frac": floor_ms / round_ms,
-                                      "floor_source": f"{n_bar} CTA barriers x {BARRIER_CYCLES} "
-                                                      "cycles (measured) at sm_mhz"}},
+            "roofline": roof,
             "round_stats": rstats,
             "clocks": clocks, "gpu_launches": int(launches)}
     if e2e:

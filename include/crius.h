@@ -331,15 +331,19 @@ crius_status crius_set_round_policy(crius_ctx *ctx, int32_t policy);
  * upload on `stream`. */
 crius_status crius_set_deadline_bounds(crius_ctx *ctx, const int64_t *t_max, void *stream);
 
-/* Counters of the last round (HOST int64 out[24]): [0] speculative Phase A
- * batches, [1] victim-sequence recomputations, [2] SM cycles in them, [3] SM
+/* Counters of the last round (HOST int64 out[32]): [0] Phase A iterations
+ * (batches), [1] victim-sequence recomputations, [2] SM cycles in them, [3] SM
  * cycles of Phase A, [4] SM cycles of Phase B, [5] admitted jobs, [6]
  * admissions through ScaleResource, [7] Phase B batches, [8..10] SM cycles of
  * the Phase A batches (direct evaluation; sequences + ScaleResource
  * evaluation; commit), [11] stale same-type move caches refreshed, [12]
  * other-type move evaluations, [13] per-type sequence invalidations, [14] 1 if
  * the admitted records lived in shared memory, [15] the round's bound on the
- * number of admitted records.  Synchronises `stream`. */
+ * number of admitted records, [16..18] SM cycles of the per-type sequence
+ * computations summed over types (preparation, moves, thresholds), [19]
+ * candidate rescans, [20] type-list entries scanned, [26] SM cycles of the
+ * commits' serial part, [28] CTA-wide barriers on the round's critical chain.
+ * Other entries are reserved (0).  Synchronises `stream`. */
 crius_status crius_round_stats(crius_ctx *ctx, int64_t *out16, void *stream);
 
 /* Number of kernels this context has launched so far (for launch accounting). */

@@ -401,14 +401,14 @@ class Crius:
     def round_stats(self, stream=None):
         out = np.zeros(32, np.int64)
         _check(lib().crius_round_stats(self.ctx, _ptr(out), _stream_handle(stream)))
-        keys = ("phaseA_batches", "seq_recomputes", "seq_cycles", "phaseA_cycles", "phaseB_cycles",
-                "admitted", "scale_admits", "phaseB_batches", "batch_direct_cycles",
-                "batch_scale_cycles", "batch_commit_cycles", "stale_caches", "other_type_evals",
-                "seq_invalidations", "records_in_smem", "records_bound", "seq_scan_cycles",
-                "seq_move_cycles", "seq_tail_cycles", "seq_rescans", "seq_entries",
-                "seq_queue_cycles", "seq_refresh_cycles", "seq_other_cycles", "seq_top2_cycles",
-                "commit_serial_cycles", "commit_tail_cycles")
-        return dict(zip(keys, (int(x) for x in out)))
+        keys = {0: "phaseA_batches", 1: "seq_recomputes", 2: "seq_cycles", 3: "phaseA_cycles",
+                4: "phaseB_cycles", 5: "admitted", 6: "scale_admits", 7: "phaseB_batches",
+                8: "batch_direct_cycles", 9: "batch_scale_cycles", 10: "batch_commit_cycles",
+                11: "stale_caches", 12: "other_type_evals", 13: "seq_invalidations",
+                14: "records_in_smem", 15: "records_bound", 16: "seq_prep_cycles",
+                17: "seq_move_cycles", 18: "seq_tail_cycles", 19: "seq_rescans", 20: "seq_entries",
+                26: "commit_serial_cycles", 28: "cta_barriers"}
+        return {k: int(out[i]) for i, k in keys.items()}
 
     def launches(self):
         return lib().crius_kernel_launches(self.ctx)

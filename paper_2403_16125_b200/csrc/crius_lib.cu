@@ -962,6 +962,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
     CK(dalloc(&c->d_free, 16));
     CK(dalloc(&c->d_total, 1));
     CK(dalloc(&c->d_round_stats, 32));
+    CK(cudaMemset(c->d_round_stats, 0, 32 * 8));
     CK(dalloc(&c->d_run_opt, J));
     CK(dalloc(&c->d_cand, J));
     CK(dalloc(&c->d_run_cell, J));

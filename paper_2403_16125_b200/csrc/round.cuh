@@ -1099,6 +1099,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
   // iteration evaluates the undecided jobs [lo, kRoundThreads) against the
   // current state and commits the first that changes it.
   long long n_batches = 0, n_seq = 0, n_scale = 0, c_seq = 0;
+  long long n_bar = 0;  // CTA-wide barriers on the round's critical chain
   long long tb = clock64();
   for (int w0 = 0; w0 < J; w0 += kRoundThreads) {
     const int q = w0 + tid;
@@ -1149,6 +1150,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
         }
       }
       __syncthreads();
+      ++n_bar;
       ++n_batches;
       if (tid == 0) {
         const long long t1 = clock64();
@@ -1169,6 +1171,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
           const long long c0 = clock64();
           if (wid < TT && ((sh.stale >> wid) & 1)) type_sequence(sh, R, A, wid);
           __syncthreads();
+      ++n_bar;
           if (tid == 0) {
             sh.stale = 0;
             sh.dmark = sh.n_adm;  // every changed record's cache is fresh again
@@ -1205,6 +1208,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
         const uint32_t b2 = __ballot_sync(0xffffffffu, k2);
         if (lane == 0) sh.wk2[wid] = b2;
         __syncthreads();
+      ++n_bar;
         if (tid == 0) {
           const long long t1 = clock64();
           sh.prof[1] += t1 - tb;
@@ -1333,6 +1337,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
         }
       }
       __syncthreads();
+      ++n_bar;
       lo = sh.lo;
       if (tid == 0) {
         const long long t1 = clock64();
@@ -1361,10 +1366,12 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
     ord[(first ? a : a - n_run) + (lo - base)] = a;
   }
   __syncthreads();
+      ++n_bar;
   long long n_bb = 0;
   for (int sweep = 0; sweep < R.depth; ++sweep) {
     if (tid == 0) sh.any_change = 0;
     __syncthreads();
+      ++n_bar;
     for (int a0 = 0; a0 < n_adm;) {
       const int a = a0 + wid < n_adm ? ord[a0 + wid] : n_adm;
       int opt = -1;
@@ -1380,6 +1387,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       }
       if (lane == 0) sh.res[wid] = opt;
       __syncthreads();
+      ++n_bar;
       if (tid == 0) {
         int f = 0;
         while (f < kRoundWarps && sh.res[f] < 0) ++f;
@@ -1400,6 +1408,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
         sh.advance = f < kRoundWarps ? f + 1 : kRoundWarps;
       }
       __syncthreads();
+      ++n_bar;
       a0 += sh.advance;
       ++n_bb;
     }
@@ -1442,8 +1451,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       R.stats[18] = sh.prof[5];
       R.stats[19] = sh.cnt[3];
       R.stats[20] = sh.cnt[4];
-      for (int k = 0; k < 3; ++k) R.stats[21 + k] = sh.prof2[k];
-      R.stats[24] = sh.prof2[3];
+      R.stats[28] = n_bar;
     }
   }
   if (tid < TT) R.free_io[tid] = sh.fr[tid];

@@ -84,6 +84,24 @@ __global__ void k_ddiv(int nwarps_active, int iters, long long *out, double *sin
   if (x == 12345.0) sink[0] = x;
 }
 
+__global__ void k_chain(int iters, long long *out, long long *sink, double *dsink) {
+  // dependent single-warp chains: int IMAD, fp64 DADD
+  long long x = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) x = x * 3 + 1;
+  long long t1 = clock64();
+  double d = 1.0 + threadIdx.x;
+  long long t2 = clock64();
+  for (int i = 0; i < iters; ++i) d = __dadd_rn(d, 0.5);
+  long long t3 = clock64();
+  if (threadIdx.x == 0) {
+    out[0] = t1 - t0;
+    out[1] = t3 - t2;
+  }
+  if (x == 12345) sink[0] = x;
+  if (d == 12345.0) dsink[0] = d;
+}
+
 int main() {
   long long *d_out, h[32];
   int *d_sink;
@@ -109,9 +127,15 @@ int main() {
     cudaMemcpy(h, d_out, 8 * 32, cudaMemcpyDeviceToHost);
     printf("ddiv chain       warps %2d : %.1f cycles/op\n", nw, h[0] / (double)it);
   }
-  k_bar<<<1, 1024>>>(it, d_out);
-  cudaMemcpy(h, d_out, 8, cudaMemcpyDeviceToHost);
-  printf("__syncthreads 1024 thr   : %.1f cycles/op\n", h[0] / (double)it);
+  for (int nt : {256, 512, 1024}) {
+    k_bar<<<1, nt>>>(it, d_out);
+    cudaMemcpy(h, d_out, 8, cudaMemcpyDeviceToHost);
+    printf("__syncthreads %4d thr   : %.1f cycles/op\n", nt, h[0] / (double)it);
+  }
+  k_chain<<<1, 32>>>(it, d_out, (long long *)d_sink, d_ds);
+  cudaMemcpy(h, d_out, 16, cudaMemcpyDeviceToHost);
+  printf("int64 IMAD chain (1 warp) : %.1f cycles/op\n", h[0] / (double)it);
+  printf("fp64 DADD chain  (1 warp) : %.1f cycles/op\n", h[1] / (double)it);
   printf("err %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
