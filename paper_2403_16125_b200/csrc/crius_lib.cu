@@ -707,7 +707,7 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   const bool craw_alias = K1e * Lp * 4 <= o - A.off_F;
   A.off_CRAW = craw_alias ? A.off_F : 0;
   A.off_BD = take(A.split_stride * 2);
-  A.off_CELL = take(3 * (maxCells + 1) * 4);
+  A.off_CELL = take(4 * (maxCells + 1) * 4);
   if (!craw_alias) A.off_CRAW = take(K1e * Lp * 4);
   A.off_NRAW = take(Lp * 4);
   A.off_POFF = take(maxCells * 8);

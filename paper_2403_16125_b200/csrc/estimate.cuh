@@ -875,6 +875,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
   int16_t *BD = (int16_t *)(base + A.off_BD);
   int32_t *CG = (int32_t *)(base + A.off_CELL);
   int32_t *CS = CG + (A.maxCells + 1), *CP = CS + (A.maxCells + 1);
+  int32_t *CK = CP + (A.maxCells + 1);  // [maxCells] smallest memory-feasible k per Cell
   int32_t *CRAW = (int32_t *)(base + A.off_CRAW);  // [K1e][Lp] raw compute rows
   int32_t *NRAW = (int32_t *)(base + A.off_NRAW);  // [Lp] raw tp_calls, then the int32 P0
   int64_t *POFF = (int64_t *)(base + A.off_POFF);  // [maxCells] raw plan offsets
@@ -1130,8 +1131,49 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
       __syncwarp();
       continue;
     }
+    // A Cell's memory use is monotone in k (mem = ceil(kst W / tp + GB A / g)
+    // shrinks as tp grows, A-13): with a microbatch sweep (NBG > 1: one (Cell,
+    // k) spans several lanes' worth of plans) its smallest feasible k, so that
+    // the plan items below skip the memory-infeasible plans instead of spending
+    // lanes on them (a Cell with none is infeasible: its record right away).
+    // With one plan per (Cell, k) the pre-pass costs more than it saves.
+    for (int ci = lane; ci < nc; ci += 32) {
+      if (NBG == 1) {
+        CK[ci] = 0;
+        continue;
+      }
+      const int G = CG[ci], S = CS[ci], lS = ilog2_pow2(S), lg = ilog2_pow2(G) - lS;
+      const int K = lg + 1;
+      const int16_t *bd = BD + (S - 1) + lS;
+      int kmin = 0;
+      int64_t pw_a = 0, pa_a = 0;
+      for (int s = 0; s < S && kmin < K; ++s) {
+        const int e = bd[s + 1];
+        const int64_t pw_e = PW[e], pa_e = PA[e];
+        const int64_t Wd = pw_e - pw_a, Ad = pa_e - pa_a;
+        while (kmin < K) {
+          const int sh = U.lGB + kmin - lg;  // GB / dp = 2^sh; dp > GB: no plan of this k
+          if (sh >= 0) {
+            const uint64_t mem = ((uint64_t)(U.kst * Wd + (Ad << sh)) + (1ull << kmin) - 1) >> kmin;
+            if (mem <= (uint64_t)U.memt) break;
+          }
+          ++kmin;
+        }
+        pw_a = pw_e;
+        pa_a = pa_e;
+      }
+      CK[ci] = kmin;
+      if (kmin == K) {
+        CellResult res;
+        res.t_ns = kInf;
+        res.plan = -1;
+        res.flags = 0;
+        emit_result(A, cb + ci, out_cell_base, res);
+      }
+    }
+    __syncwarp();
     // processing order: Cells by S descending (stable) so a 32-lane chunk runs
-    // stage loops of one length; item = (Cell, k, group of NBG microbatch counts)
+    // stage loops of one length; item = (Cell, k >= kmin, group of NBG microbatch counts)
     const int ngrp = P.b_mode == 0 ? 1 : (P.nB + NBG - 1) / NBG;
     const bool sorted = npu / P.nB * ngrp > 32;  // one chunk: order does not matter
     for (int i = lane; i < nc; i += 32) {
@@ -1151,7 +1193,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
         int cnt = 0;
         if (r < nc) {
           const int ci = ORD[r];
-          cnt = (ilog2_pow2(CG[ci] / CS[ci]) + 1) * ngrp;
+          cnt = (ilog2_pow2(CG[ci] / CS[ci]) + 1 - CK[ci]) * ngrp;
         }
         const int inc = warp_incl_scan32(cnt, lane);
         if (r < nc) CP[r + 1] = carry + inc;
@@ -1181,7 +1223,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
         r = lo;
         const int ci = ORD[r], local = f - CP[r];
         CRIUS_CHECK(ci >= 0 && ci < nc && local >= 0 && local < CP[r + 1] - CP[r]);
-        const int kk = NBG == 1 ? local : local / ngrp, gg = NBG == 1 ? 0 : local - kk * ngrp;
+        const int kl = NBG == 1 ? local : local / ngrp, gg = NBG == 1 ? 0 : local - kl * ngrp;
+        const int kk = CK[ci] + kl;
         if (NBG == 1) {  // one microbatch count per lane: the per-plan evaluation
           p = P.b_mode == 0 ? kk : kk * P.nB + gg;
           T = plan_time(U, CG[ci], CS[ci], p);
