@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-1 evidence, session 2 (tag = $1): bench lines, reference arm, launch list, full captures
+# evidence (tag = $1): bench lines, reference arm, launch list, full captures of k_estimate / k_round
 cd $GRAFT_REPO_ROOT
 P=gpurun_out/$1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > ${P}_smi.txt 2>&1
@@ -14,7 +14,7 @@ timeout 300 python bench.py --assembly 1 --form 1 --steps 5 --warmup 3 --no-cpu-
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-flush"
 timeout 200 $CMD > ${P}_plain.log 2>&1 && \
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${P}_launches.csv $CMD > ${P}_ncu1.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_estimate|k_round_greedy" -s 2 -c 2 -o ${P}_full $CMD > ${P}_ncu2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"k_estimate|7k_roundI" -s 2 -c 2 -o ${P}_full $CMD > ${P}_ncu2.log 2>&1
 CMD5="python scripts/est_bench.py --configs 5 --reps 1"
 timeout 200 $CMD5 > ${P}_plain5.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_estimate" -s 1 -c 1 -o ${P}_full5 $CMD5 > ${P}_ncu3.log 2>&1
