@@ -280,6 +280,7 @@ struct RoundShared {
   int32_t toff[kRT + 1], tn[kRT];
   unsigned long long tcap[kRT];  // free + GPUs held by running jobs, per type
   int32_t n_adm, advance, any_change, lo;
+  int32_t max_adm;           // the round's bound on the admitted records
   int32_t p_used, p_cap;     // option pool entries used / available
   int32_t po_first;          // pool offset of the first record of the current commit
   int32_t dmark;             // records [dmark, n_adm) were admitted since the last recompute
@@ -305,6 +306,7 @@ __device__ __forceinline__ void list_remove(RoundShared &sh, const AdmView &A, i
   A.slot[last] = s;
 }
 __device__ __forceinline__ void list_add(RoundShared &sh, const AdmView &A, int a, int u) {
+  CRIUS_CHECK(sh.tn[u] < sh.toff[u + 1] - sh.toff[u]);
   int32_t *tl = A.tl + sh.toff[u];
   const int s = sh.tn[u]++;
   tl[s] = a;
@@ -851,6 +853,8 @@ __device__ __forceinline__ void adm_point(RoundShared &sh, const AdmView &A, int
 __device__ __forceinline__ void adm_new(RoundShared &sh, const AdmView &A, int w, int pos, int idx,
                                         int G, int t, int po) {
   const int a = sh.n_adm++;
+  CRIUS_CHECK(a < sh.max_adm && idx < sh.bs_nopt[w]);
+  CRIUS_CHECK(po < 0 || po + sh.bs_nopt[w] <= sh.p_cap);
   const uint64_t gb = sh.bs_gmb[w];
   A.gmb[a] = gb;
   A.tsb[a] = sh.bs_tsb[w];
@@ -1014,6 +1018,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       sh.tn[u] = 0;
     }
     sh.toff[TT] = o;
+    sh.max_adm = max_adm;
     sh.p_used = 0;
     sh.p_cap = pcap;
   }
@@ -1252,6 +1257,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
               sh.vic[sh.n_vic + lane] = a;
             }
             const int an = a_new;
+            CRIUS_CHECK(an < sh.max_adm && res_idx(rr) < sh.bs_nopt[f] && m <= S.len);
             switch (lane) {
               case 0: A.pos[an] = w0 + f; break;
               case 1: A.cur[an] = res_idx(rr); break;
