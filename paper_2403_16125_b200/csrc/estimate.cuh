@@ -1131,17 +1131,15 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
       __syncwarp();
       continue;
     }
+    const int ngrp = P.b_mode == 0 ? 1 : (P.nB + NBG - 1) / NBG;
     // A Cell's memory use is monotone in k (mem = ceil(kst W / tp + GB A / g)
     // shrinks as tp grows, A-13): with a microbatch sweep (NBG > 1: one (Cell,
     // k) spans several lanes' worth of plans) its smallest feasible k, so that
     // the plan items below skip the memory-infeasible plans instead of spending
     // lanes on them (a Cell with none is infeasible: its record right away).
     // With one plan per (Cell, k) the pre-pass costs more than it saves.
-    for (int ci = lane; ci < nc; ci += 32) {
-      if (NBG == 1) {
-        CK[ci] = 0;
-        continue;
-      }
+    for (int ci = lane; ci < nc && NBG == 1; ci += 32) CK[ci] = 0;
+    for (int ci = lane; ci < nc && NBG > 1; ci += 32) {
       const int G = CG[ci], S = CS[ci], lS = ilog2_pow2(S), lg = ilog2_pow2(G) - lS;
       const int K = lg + 1;
       const int16_t *bd = BD + (S - 1) + lS;
@@ -1174,7 +1172,6 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
     __syncwarp();
     // processing order: Cells by S descending (stable) so a 32-lane chunk runs
     // stage loops of one length; item = (Cell, k >= kmin, group of NBG microbatch counts)
-    const int ngrp = P.b_mode == 0 ? 1 : (P.nB + NBG - 1) / NBG;
     const bool sorted = npu / P.nB * ngrp > 32;  // one chunk: order does not matter
     for (int i = lane; i < nc; i += 32) {
       int r = i;
