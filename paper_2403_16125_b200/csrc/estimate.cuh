@@ -171,7 +171,7 @@ __device__ __forceinline__ uint64_t ceil_shr128(uint64_t hi, uint64_t lo, int e)
 // so every alpha-beta term is a 128-bit product formed once per stage (tpc: X,
 // boundary send: Y, boundary all-gather: Z) followed, per B, by an exact
 // ceil-shift.  Returns the best (T, p) of the group (lowest p on ties).
-template <int NBG>
+template <int NBG, bool kMemFeasible = false>
 __device__ __forceinline__ int64_t plan_group_time(const UnitCtx &U, int G, int S, int k, int bg,
                                                    int &best_p) {
   const int lS = ilog2_pow2(S), lg = ilog2_pow2(G) - lS;
@@ -205,9 +205,13 @@ __device__ __forceinline__ int64_t plan_group_time(const UnitCtx &U, int G, int 
     const int e = bd[s + 1];
     const int64_t pc_e = PCk[e], pv_e = U.PV[e], pn_e = U.PN[e], pw_e = U.PW[e], pa_e = U.PA[e];
     const int64_t W = pw_e - pw_a, A = pa_e - pa_a, C = pc_e - pc_a;
-    // mem = cdiv(kst W + (GB/dp) A, tp) <= mem_t  (A-13): B-independent
-    const uint64_t mem = ((uint64_t)(U.kst * W + (A << (U.lGB - ldp))) + tp - 1) >> k;
-    if (mem > (uint64_t)U.memt) return kInf;
+    // mem = cdiv(kst W + (GB/dp) A, tp) <= mem_t  (A-13): B-independent;
+    // the plain estimator's items start at the Cell's smallest memory-feasible k
+    // (memory is monotone in k), so only the other modes check it here
+    if (!kMemFeasible) {
+      const uint64_t mem = ((uint64_t)(U.kst * W + (A << (U.lGB - ldp))) + tp - 1) >> k;
+      if (mem > (uint64_t)U.memt) return kInf;
+    }
     // sync = AR(dp, l_dp, cdiv(W, tp), 1): B-independent
     if (ldp) {
       const uint64_t Wt = ((uint64_t)W + tp - 1) >> k;
@@ -1226,7 +1230,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
           p = P.b_mode == 0 ? kk : kk * P.nB + gg;
           T = plan_time(U, CG[ci], CS[ci], p);
         } else {
-          T = plan_group_time<NBG>(U, CG[ci], CS[ci], kk, gg, p);
+          T = plan_group_time<NBG, true>(U, CG[ci], CS[ci], kk, gg, p);
         }
       }
       // segmented inclusive min-scan over (T, p); left lanes have lower p
