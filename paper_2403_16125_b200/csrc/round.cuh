@@ -276,7 +276,7 @@ struct SeqTab {
 };
 
 struct RoundShared {
-  int32_t fr[kRT], old_fr[kRT];
+  int32_t fr[kRT];
   int32_t toff[kRT + 1], tn[kRT];
   unsigned long long tcap[kRT];  // free + GPUs held by running jobs, per type
   int32_t n_adm, advance, any_change, lo;
@@ -783,26 +783,24 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
 // the types one of whose jobs has an option on a type whose free count changed
 // and that fits under the old or the new count (that changes its other-type
 // moves).
-__device__ __forceinline__ void invalidate(RoundShared &sh, int TT, uint32_t changed, int policy) {
+__device__ __forceinline__ void invalidate(RoundShared &sh, int TT, uint32_t changed, int o_q, int n_q,
+                                           int policy) {
+  // lane q holds type q's free count before (o_q) and after (n_q) the commit
   const int u = threadIdx.x & 31;
-  bool bad = false;
-  if (u < TT && !((sh.stale >> u) & 1)) {
-    bad = (changed >> u) & 1;
-    if (!(policy & 2)) {
-      const uint64_t gq = sh.sq[u].gq;
-      const uint32_t iit = sh.sq[u].iit;
-      for (int q = 0; q < TT && !bad; ++q) {
-        const int o = sh.old_fr[q], n = sh.fr[q];
-        if (q == u || o == n) continue;
-        if (n < o) {
-          // fewer free GPUs on q only removes or worsens other-type moves to q:
-          // the argmins of a sequence that made no move to q stand
-          bad = (iit >> q) & 1;
-        } else {
-          const int g = byte_of(gq, q);
-          bad = g != 0xff && (1 << g) <= n;
-        }
-      }
+  bool bad = u < TT && !((sh.stale >> u) & 1) && ((changed >> u) & 1);
+  const bool chk = u < TT && !((sh.stale >> u) & 1) && !(policy & 2);
+  const uint64_t gq = u < TT ? sh.sq[u].gq : ~0ull;
+  const uint32_t iit = u < TT ? sh.sq[u].iit : 0u;
+  for (int q = 0; q < TT; ++q) {
+    const int o = __shfl_sync(0xffffffffu, o_q, q), n = __shfl_sync(0xffffffffu, n_q, q);
+    if (!chk || bad || q == u || o == n) continue;
+    if (n < o) {
+      // fewer free GPUs on q only removes or worsens other-type moves to q:
+      // the argmins of a sequence that made no move to q stand
+      bad = (iit >> q) & 1;
+    } else {
+      const int g = byte_of(gq, q);
+      bad = g != 0xff && (1 << g) <= n;
     }
   }
   const uint32_t m = __ballot_sync(0xffffffffu, bad);
@@ -1220,62 +1218,64 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
           tb = t1;
         }
       }
-      // (3) commit the first job f that changes the state: thread 0 updates the
-      // records and free counts while warp 1 stages job f's options in the pool
-      if (wid <= 1) {
+      // (3) commit the first job f that changes the state: warp 0 updates the
+      // records and free counts, warp 1 stages job f's options in the pool, and
+      // (ScaleResource) warp 2 invalidates the sequences meanwhile -- every
+      // input of that is in the sequence and the result word
+      if (wid <= 2) {
         const int f2n = nb ? first_bit(sh.wk2) : kRoundThreads;
         const int f = min(fa, f2n);
-        if (wid == 1) {
-          if (lane == 0) sh.po_first = f < kRoundThreads ? pool_alloc(sh, sh.bs_nopt[f]) : -1;
-          asm volatile("bar.sync 1, 64;" ::: "memory");
-          if (f < kRoundThreads && sh.po_first >= 0) stage_job(R, A, w0 + f, sh.bs_nopt[f], sh.po_first);
-        } else {
-          asm volatile("bar.sync 1, 64;" ::: "memory");
-          const long long k0 = tstamp();
-          const int a_new = sh.n_adm;
-          if (f < kRoundThreads && f2n < fa) {
-            // ScaleResource (lanes in parallel): the first m moves of the type's
-            // sequence (lane mm updates victim mm), the free counts (lane u),
-            // then job f's record on its option (one field per lane)
+        const bool scale = f < kRoundThreads && f2n < fa;
+        if (wid == 2) {
+          const int o = lane < TT ? sh.fr[lane] : 0;  // nobody writes them before bar 1
+          asm volatile("bar.sync 1, 96;" ::: "memory");
+          if (scale) {
             const int rr = sh.res[f], t = res_t(rr), m = res_m(rr), G = res_G(rr);
             const SeqTab &S = sh.sq[t];
-            if (lane < TT) {
-              const int o = sh.fr[lane];
-              sh.old_fr[lane] = o;
-              sh.fr[lane] = o + S.dfr[m][lane] - (lane == t ? G : 0);
-            }
-            uint32_t ch = 0;
+            const int n = lane < TT ? o + S.dfr[m][lane] - (lane == t ? G : 0) : 0;
+            // the victims are type-t jobs; the other-type ones land on t2
+            const uint32_t ch = lane < m ? 1u << ((S.mv_pk[lane] >> 16) & 0xff) : 0u;
+            invalidate(sh, TT, __reduce_or_sync(0xffffffffu, ch) | (1u << t), o, n, R.policy);
+          }
+        } else if (wid == 1) {
+          if (lane == 0) sh.po_first = f < kRoundThreads ? pool_alloc(sh, sh.bs_nopt[f]) : -1;
+          asm volatile("bar.sync 1, 96;" ::: "memory");
+          if (f < kRoundThreads && sh.po_first >= 0) stage_job(R, A, w0 + f, sh.bs_nopt[f], sh.po_first);
+        } else {
+          asm volatile("bar.sync 1, 96;" ::: "memory");
+          const int a_new = sh.n_adm;
+          const int old = lane < TT ? sh.fr[lane] : 0;  // free counts before the commit
+          if (scale) {
+            // ScaleResource: the first m moves of the type's sequence (lane mm
+            // updates victim mm), the free counts (lane u), then job f's record
+            const int rr = sh.res[f], t = res_t(rr), m = res_m(rr), G = res_G(rr);
+            const SeqTab &S = sh.sq[t];
+            if (lane < TT) sh.fr[lane] = old + S.dfr[m][lane] - (lane == t ? G : 0);
             bool moved_type = false;
             if (lane < m) {
               const int a = S.mv_a[lane], pk = S.mv_pk[lane];
-              const int t2 = (pk >> 16) & 0xff, ta = A.t[a];
-              ch = (1u << ta) | (1u << t2);
-              moved_type = ta != t2;
+              moved_type = ((pk >> 16) & 0xff) != t;
               A.cur[a] = pk & 0xff;
               A.G[a] = 1 << ((pk >> 8) & 0xff);
               A.bi[a] = -2;
               sh.vic[sh.n_vic + lane] = a;
             }
-            const int an = a_new;
-            CRIUS_CHECK(an < sh.max_adm && res_idx(rr) < sh.bs_nopt[f] && m <= S.len);
-            switch (lane) {
-              case 0: A.pos[an] = w0 + f; break;
-              case 1: A.cur[an] = res_idx(rr); break;
-              case 2: A.G[an] = G; break;
-              case 3: A.t[an] = t; break;
-              case 4: A.bi[an] = -2; break;
-              case 5: A.ei[an] = -1; break;
-              case 6: A.gmb[an] = sh.bs_gmb[f]; break;
-              case 7: A.tsb[an] = sh.bs_tsb[f]; break;
-              case 8: A.nopt[an] = sh.bs_nopt[f]; break;
-              case 9: A.po[an] = sh.po_first; break;
-              default: break;
-            }
-            const uint32_t cm = __reduce_or_sync(0xffffffffu, ch) | (1u << t);
             const uint32_t mt = __ballot_sync(0xffffffffu, moved_type);
             __syncwarp();
             if (lane == 0) {
               ++n_scale;
+              const int an = a_new;
+              CRIUS_CHECK(an < sh.max_adm && res_idx(rr) < sh.bs_nopt[f] && m <= S.len);
+              A.pos[an] = w0 + f;
+              A.cur[an] = res_idx(rr);
+              A.G[an] = G;
+              A.t[an] = t;
+              A.bi[an] = -2;
+              A.ei[an] = -1;
+              A.gmb[an] = sh.bs_gmb[f];
+              A.tsb[an] = sh.bs_tsb[f];
+              A.nopt[an] = sh.bs_nopt[f];
+              A.po[an] = sh.po_first;
               // victims that changed type move between the type lists
               for (uint32_t b = mt; b; b &= b - 1) {
                 const int mm = __ffs(b) - 1;
@@ -1289,56 +1289,50 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
               sh.n_adm = an + 1;
               list_add(sh, A, an, t);
               gq_join(sh, t, sh.bs_gmb[f]);
-              sh.changed = cm;
               sh.lo = f + 1;
             }
-          } else if (lane == 0) {
-            int adv = kRoundThreads;
-            if (f < kRoundThreads) {  // direct admissions, chained while later choices provably stand
-              for (int u = 0; u < TT; ++u) sh.old_fr[u] = sh.fr[u];
-              uint32_t changed = 0;
-              int w = f;
-              for (;;) {
-                const int rr = sh.res[w], t = res_t(rr);
-                adm_new(sh, A, w, w0 + w, res_idx(rr), res_G(rr), t,
-                        w == f ? sh.po_first : pool_alloc(sh, sh.bs_nopt[w]));
-                sh.fr[t] -= res_G(rr);
-                changed |= 1u << t;
-                adv = w + 1;
-                // A direct admission only lowers one free count, so a later job's
-                // direct choice stands iff its option still fits; a job that stays
-                // pending without ScaleResource is unaffected.
-                bool more = false;
-                while (++w < kRoundThreads && w0 + w < J) {
-                  const bool wk = (sh.wk1[w >> 5] >> (w & 31)) & 1;
-                  const bool wn = (sh.wnd[w >> 5] >> (w & 31)) & 1;
-                  if (wk) {
-                    const int r2 = sh.res[w];
-                    more = res_G(r2) <= sh.fr[res_t(r2)];
+          } else {
+            uint32_t changed = 0;
+            if (lane == 0) {
+              int adv = kRoundThreads;
+              if (f < kRoundThreads) {  // direct admissions, chained while later choices provably stand
+                int w = f;
+                for (;;) {
+                  const int rr = sh.res[w], t = res_t(rr);
+                  adm_new(sh, A, w, w0 + w, res_idx(rr), res_G(rr), t,
+                          w == f ? sh.po_first : pool_alloc(sh, sh.bs_nopt[w]));
+                  sh.fr[t] -= res_G(rr);
+                  changed |= 1u << t;
+                  adv = w + 1;
+                  // A direct admission only lowers one free count, so a later job's
+                  // direct choice stands iff its option still fits; a job that stays
+                  // pending without ScaleResource is unaffected.
+                  bool more = false;
+                  while (++w < kRoundThreads && w0 + w < J) {
+                    const bool wk = (sh.wk1[w >> 5] >> (w & 31)) & 1;
+                    const bool wn = (sh.wnd[w >> 5] >> (w & 31)) & 1;
+                    if (wk) {
+                      const int r2 = sh.res[w];
+                      more = res_G(r2) <= sh.fr[res_t(r2)];
+                      break;
+                    }
+                    if (!wn) {
+                      adv = w + 1;
+                      continue;
+                    }
                     break;
                   }
-                  if (!wn) {
-                    adv = w + 1;
-                    continue;
-                  }
-                  break;
+                  if (!more) break;
                 }
-                if (!more) break;
               }
-              sh.changed = changed;
+              sh.lo = adv;
             }
-            sh.lo = adv;
-          }
-          __syncwarp();
-          const long long k1 = tstamp();
-          if (f < kRoundThreads) {
-            invalidate(sh, TT, sh.changed, R.policy);
-            stage_options(R, A, a_new + 1, sh.n_adm);  // the chain's later records
-          }
-          __syncwarp();
-          if (lane == 0) {
-            sh.prof[6] += k1 - k0;
-            sh.prof[7] += tstamp() - k1;
+            __syncwarp();
+            if (f < kRoundThreads) {
+              invalidate(sh, TT, __shfl_sync(0xffffffffu, changed, 0), old, lane < TT ? sh.fr[lane] : 0,
+                         R.policy);
+              stage_options(R, A, a_new + 1, sh.n_adm);  // the chain's later records
+            }
           }
         }
       }
@@ -1450,8 +1444,6 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       R.stats[13] = sh.cnt[2];
       R.stats[14] = in_smem;
       R.stats[15] = max_adm;
-      R.stats[26] = sh.prof[6];
-      R.stats[27] = sh.prof[7];
       R.stats[16] = sh.prof[3];
       R.stats[17] = sh.prof[4];
       R.stats[18] = sh.prof[5];
