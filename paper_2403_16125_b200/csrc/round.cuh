@@ -333,15 +333,19 @@ __device__ __forceinline__ void opt_get(const RoundBuf &R, const AdmView &A, int
 
 // One lane: the job's best same-type move (case i): argmin over its options on
 // its type with smaller G (indices [first of type, cur) in (t, G) order) of
-// key = (score(cur) - score(o')) / (G_cur - G_o'), ties -> lowest index.
-__device__ __forceinline__ void refresh_i(const RoundBuf &R, const AdmView &A, int a) {
-  const int p = A.pos[a], cv = A.cur[a], Gc = A.G[a], tt = A.t[a], po = A.po[a];
-  const int i0 = byte_of(A.tsb[a], tt);
+// key = (score(cur) - score(o')) / (G_cur - G_o'), ties -> lowest index.  The
+// core takes the record's fields explicitly (the commit refreshes the records
+// it changes while their fields are being written).
+__device__ __forceinline__ void refresh_core(const RoundBuf &R, const AdmView &A, int p, int cv, int Gc,
+                                             int tt, int po, uint64_t tsb, int &bi, double &bk,
+                                             double &bl) {
+  const int i0 = byte_of(tsb, tt);
   int lg, t2;
   double sc;
   opt_get(R, A, po, p, cv, lg, t2, sc);
-  int bi = -1;
-  double bk = 0.0, bl = 0.0;
+  bi = -1;
+  bk = 0.0;
+  bl = 0.0;
 #pragma unroll 4
   for (int i2 = i0; i2 < cv; ++i2) {  // ascending: strict < keeps the lowest index on ties
     double s2;
@@ -354,6 +358,11 @@ __device__ __forceinline__ void refresh_i(const RoundBuf &R, const AdmView &A, i
       bl = l;
     }
   }
+}
+__device__ __forceinline__ void refresh_i(const RoundBuf &R, const AdmView &A, int a) {
+  int bi;
+  double bk, bl;
+  refresh_core(R, A, A.pos[a], A.cur[a], A.G[a], A.t[a], A.po[a], A.tsb[a], bi, bk, bl);
   A.bi[a] = bi;
   A.bk[a] = bk;
   A.bl[a] = bl;
@@ -556,8 +565,11 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   bool all = S.tall != 0;
   TopLane x{S.tk[lane], S.tlo[lane], S.tt[lane], S.ta[lane], S.tp[lane]};
   {
-    bool ok = lane < cnt;
-    if (ok) ok = A.t[x.a] == t && A.bi[x.a] != -2;
+    bool ok = lane < cnt;  // records admitted since the last recompute are in no list
+    if (ok) {
+      ok = A.t[x.a] == t;
+      for (int i = 0; i < sh.n_vic; ++i) ok &= sh.vic[i] != x.a;
+    }
     const uint32_t m = __ballot_sync(0xffffffffu, ok);
     if (m != (cnt >= 32 ? 0xffffffffu : (1u << cnt) - 1)) {
       const int nc = __popc(m);
@@ -578,11 +590,11 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
       int a = -1;
       if (k < d1 - d0) a = d0 + k;
       else if (k < d1 - d0 + nv) a = sh.vic[k - (d1 - d0)];
-      const bool mine = a >= 0 && A.t[a] == t && A.bi[a] == -2;
+      const bool mine = a >= 0 && A.t[a] == t;
       const uint32_t mm = __ballot_sync(0xffffffffu, mine);
       if (mine && nd + __popc(mm & ((1u << lane) - 1)) < kQ) qd[nd + __popc(mm & ((1u << lane) - 1))] = a;
       nd += __popc(mm);
-      if (mine) refresh_i(R, A, a);  // lanes in parallel
+      if (mine && A.bi[a] == -2) refresh_i(R, A, a);  // lanes in parallel (a commit refreshed the rest)
     }
     __syncwarp();
     n_ref = nd;
@@ -1220,15 +1232,16 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       }
       // (3) commit the first job f that changes the state: warp 0 updates the
       // records and free counts, warp 1 stages job f's options in the pool, and
-      // (ScaleResource) warp 2 invalidates the sequences meanwhile -- every
-      // input of that is in the sequence and the result word
-      if (wid <= 2) {
+      // (ScaleResource) warp 2 invalidates the sequences and warp 3 refreshes
+      // the changed records' same-type caches meanwhile -- every input of that
+      // is in the sequence and the result word
+      if (wid <= 3) {
         const int f2n = nb ? first_bit(sh.wk2) : kRoundThreads;
         const int f = min(fa, f2n);
         const bool scale = f < kRoundThreads && f2n < fa;
         if (wid == 2) {
           const int o = lane < TT ? sh.fr[lane] : 0;  // nobody writes them before bar 1
-          asm volatile("bar.sync 1, 96;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
           if (scale) {
             const int rr = sh.res[f], t = res_t(rr), m = res_m(rr), G = res_G(rr);
             const SeqTab &S = sh.sq[t];
@@ -1239,10 +1252,44 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
           }
         } else if (wid == 1) {
           if (lane == 0) sh.po_first = f < kRoundThreads ? pool_alloc(sh, sh.bs_nopt[f]) : -1;
-          asm volatile("bar.sync 1, 96;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
           if (f < kRoundThreads && sh.po_first >= 0) stage_job(R, A, w0 + f, sh.bs_nopt[f], sh.po_first);
+        } else if (wid == 3) {
+          const int an = sh.n_adm;  // nobody writes it before bar 1
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (scale) {
+            const int rr = sh.res[f], t = res_t(rr), m = res_m(rr);
+            const SeqTab &S = sh.sq[t];
+            int a = -1, p = 0, cv = 0, Gc = 0, tt = 0, po = -1;
+            uint64_t tsb = 0;
+            if (lane < m) {  // victim: its new option; pos, po, tsb do not change
+              const int pk = S.mv_pk[lane];
+              a = S.mv_a[lane];
+              p = A.pos[a];
+              po = A.po[a];
+              tsb = A.tsb[a];
+              cv = pk & 0xff;
+              Gc = 1 << ((pk >> 8) & 0xff);
+              tt = (pk >> 16) & 0xff;
+            } else if (lane == m) {  // the new record (its pool copy is being staged: global path)
+              a = an;
+              p = w0 + f;
+              tsb = sh.bs_tsb[f];
+              cv = res_idx(rr);
+              Gc = res_G(rr);
+              tt = t;
+            }
+            if (a >= 0) {
+              int bi;
+              double bk, bl;
+              refresh_core(R, A, p, cv, Gc, tt, po, tsb, bi, bk, bl);
+              A.bi[a] = bi;
+              A.bk[a] = bk;
+              A.bl[a] = bl;
+            }
+          }
         } else {
-          asm volatile("bar.sync 1, 96;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
           const int a_new = sh.n_adm;
           const int old = lane < TT ? sh.fr[lane] : 0;  // free counts before the commit
           if (scale) {
@@ -1256,8 +1303,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
               const int a = S.mv_a[lane], pk = S.mv_pk[lane];
               moved_type = ((pk >> 16) & 0xff) != t;
               A.cur[a] = pk & 0xff;
-              A.G[a] = 1 << ((pk >> 8) & 0xff);
-              A.bi[a] = -2;
+              A.G[a] = 1 << ((pk >> 8) & 0xff);  // bi: warp 3 writes the refreshed cache
               sh.vic[sh.n_vic + lane] = a;
             }
             const uint32_t mt = __ballot_sync(0xffffffffu, moved_type);
@@ -1270,7 +1316,6 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
               A.cur[an] = res_idx(rr);
               A.G[an] = G;
               A.t[an] = t;
-              A.bi[an] = -2;
               A.ei[an] = -1;
               A.gmb[an] = sh.bs_gmb[f];
               A.tsb[an] = sh.bs_tsb[f];
