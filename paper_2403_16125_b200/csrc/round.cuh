@@ -118,23 +118,33 @@ __device__ __forceinline__ bool kappa_less(const OptRec &a, const OptRec &b) {
 
 // K5: per job (thread), options, ref and scores from its Cells (contiguous,
 // (t, G, S) order), written at the job's priority position; the arrival
-// options in kappa order; per-type smallest G and first index.
-__global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
-                                const int32_t *__restrict__ cType, const int32_t *__restrict__ cG,
-                                const CellResult *__restrict__ res, RoundBuf R) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= R.J) return;
+// options in kappa order; per-type smallest G and first index.  The options
+// are built in a thread-local buffer (OB: kLocalOpt entries, L1-resident) when
+// they fit, else in place in the global table.
+constexpr int kLocalOpt = 32;
+template <bool kLocal>
+__device__ __forceinline__ void round_options_job(const Params &P, const int64_t *__restrict__ ucb,
+                                                  const int32_t *__restrict__ cType,
+                                                  const int32_t *__restrict__ cG,
+                                                  const CellResult *__restrict__ res, const RoundBuf &R,
+                                                  int j) {
   const int pos = R.rank[j];
   const int64_t c0 = ucb[(int64_t)j * R.T], c1 = ucb[(int64_t)(j + 1) * R.T];
   const int ngj = P.ng[j];
-  OptRec *o = R.opt + (int64_t)pos * R.maxopt;
-  int64_t *oc = R.opt_cell + (int64_t)pos * R.maxopt;
+  OptRec *og = R.opt + (int64_t)pos * R.maxopt;
+  int64_t *ocg = R.opt_cell + (int64_t)pos * R.maxopt;
+  OptRec ol[kLocal ? kLocalOpt : 1];
+  int64_t ocl[kLocal ? kLocalOpt : 1];
+  OptRec *o = kLocal ? ol : og;
+  int64_t *oc = kLocal ? ocl : ocg;
   int n = 0;
   int64_t ref_ng = kInf, ref_any = kInf;
   int lastT = -1, lastG = -1;
   const bool act = R.active ? R.active[j] != 0 : true;
   const int64_t rc0 = (act && R.run_cell) ? R.run_cell[j] : -1;
+  const int rct = rc0 >= 0 ? cType[rc0] : -1, rcG = rc0 >= 0 ? cG[rc0] : -1;
   const int64_t tmx = R.tmax ? R.tmax[j] : kInf;
+#pragma unroll 4
   for (int64_t c = c0; c < c1; ++c) {
     const int64_t T = res[c].t_ns;
     const int t = cType[c], G = cG[c];
@@ -144,7 +154,7 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
     if ((R.policy & 1) && G != ngj) continue;  // NA: the job stays at N_G GPUs
     // deadline: a Cell slower than the job's bound is no option, except the
     // (type, G) the job runs on (its completion was guaranteed at placement)
-    if (T > tmx && !(rc0 >= 0 && t == cType[rc0] && G == cG[rc0])) continue;
+    if (T > tmx && !(t == rct && G == rcG)) continue;
     if (t == lastT && G == lastG) {
       if (T < o[n - 1].T) {  // equal T keeps the earlier (smaller S) Cell
         o[n - 1].T = T;
@@ -164,10 +174,15 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
   double *sc = R.score + (int64_t)pos * R.maxopt;
   uint64_t gmb = ~0ull, tsv = ~0ull;
   for (int i = 0; i < n; ++i) {
-    sc[i] = score_of(ref, o[i].T);
-    const int sh = 8 * o[i].t;
+    const OptRec x = o[i];
+    if (kLocal) {
+      og[i] = x;
+      ocg[i] = oc[i];
+    }
+    sc[i] = score_of(ref, x.T);
+    const int sh = 8 * x.t;
     if (((gmb >> sh) & 0xff) == 0xff) {  // first (smallest G) option of its type
-      gmb = (gmb & ~(0xffull << sh)) | ((uint64_t)ilog2_pow2((uint32_t)o[i].G) << sh);
+      gmb = (gmb & ~(0xffull << sh)) | ((uint64_t)ilog2_pow2((uint32_t)x.G) << sh);
       tsv = (tsv & ~(0xffull << sh)) | ((uint64_t)i << sh);
     }
   }
@@ -184,7 +199,7 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
       r += (y.G <= ngj && kappa_less(y, x));
     }
     R.ao_pk[(int64_t)r * R.J + pos] = i | (ilog2_pow2((uint32_t)x.G) << 8) | (x.t << 13);
-    R.ao_sc[(int64_t)r * R.J + pos] = sc[i];
+    R.ao_sc[(int64_t)r * R.J + pos] = score_of(ref, x.T);
     ++na;
   }
   R.nao[pos] = na;
@@ -193,14 +208,24 @@ __global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
   R.cur[pos] = -1;
   // round state: a running job keeps the option of its Cell's (type, G)
   int ro = -1;
-  if (act && R.run_cell && R.run_cell[j] >= 0) {
-    const int64_t rc = R.run_cell[j];
+  if (rc0 >= 0) {
     for (int i = 0; i < n; ++i)
-      if (o[i].t == cType[rc] && o[i].G == cG[rc]) ro = i;
+      if (o[i].t == rct && o[i].G == rcG) ro = i;
     if (ro < 0) atomicExch(R.err, 1);  // the oracle rejects this input (status 2)
   }
   R.run_opt[pos] = ro;
   R.cand[pos] = (int8_t)(act && ro < 0 && ref != kInf && na > 0);
+}
+
+__global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
+                                const int32_t *__restrict__ cType, const int32_t *__restrict__ cG,
+                                const CellResult *__restrict__ res, RoundBuf R) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= R.J) return;
+  if (R.maxopt <= kLocalOpt)
+    round_options_job<true>(P, ucb, cType, cG, res, R, j);
+  else
+    round_options_job<false>(P, ucb, cType, cG, res, R, j);
 }
 
 // ---- warp argmin by lexicographic 3-word keys, one redux.sync per word ------
