@@ -114,6 +114,10 @@ __device__ __forceinline__ int warp_max_int(int x) {
   return __reduce_max_sync(0xffffffffu, x);  // redux.sync: one instruction, no shuffle rounds
 }
 
+__device__ __forceinline__ int warp_sum_int(int x) {
+  return (int)__reduce_add_sync(0xffffffffu, (unsigned)x);
+}
+
 // Warp-wide inclusive scan of int32 values (one shuffle per step).
 __device__ __forceinline__ int warp_incl_scan32(int x, int lane) {
 #pragma unroll

@@ -717,6 +717,10 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   A.off_PS = take(amode == 4 ? Lp * 12 + Stop * 4 : 0);
   A.warp_bytes = o;
   const int64_t nunits = unit_end - unit_begin;
+  // per-stage plan lanes when units hold few plans (cfg4: 21 per unit, 0.25 ->
+  // 0.23 ms; the all-pow2 variant's 132 per unit: 0.65 -> 0.85 ms, so per plan)
+  A.per_stage = c->P.b_mode == 0 && c->n_plans <= 48 * c->n_units;
+  if (const char *e = getenv("CRIUS_EST_PER_STAGE")) A.per_stage = c->P.b_mode == 0 && atoi(e) != 0;
   CK(cudaMemsetAsync(c->d_counter, 0, 4, st));
   int warps = 4;
   if (4 * A.warp_bytes > 200 * 1024) warps = 1;

@@ -51,6 +51,7 @@ struct EstArgs {
   CellResult *xout[kMaxRanks];
   int64_t *xflag[kMaxRanks];
   uint32_t *x_done;        // CTA completion counter (the last CTA resets it)
+  int32_t per_stage;       // b_mode 0 plan evaluation: one (Cell, k, stage) per lane
 };
 
 // One Cell record: to the caller's chunk (local index) and, with the fused
@@ -852,12 +853,13 @@ __device__ __forceinline__ UnitMeta load_meta(const Params &P, const EstArgs &A,
 }
 
 #ifndef CRIUS_EST_MINB
-#define CRIUS_EST_MINB 4  // <= 128 registers: 4 CTAs (16 warps) per SM
+#define CRIUS_EST_MINB 6  // <= 80 registers: 6 CTAs (24 warps) per SM
 #endif
 // The B-sweep instantiation (NBG > 1) keeps NBG partial sums per lane and spills
 // at 128 registers; its per-warp shared memory already caps it near 3 CTAs per
 // SM at large L, so it gets <= 168 registers (measured: cfg5 4.80 -> 4.34 ms,
-// cfg3 0.129 -> 0.123 ms; the NBG = 1 kernel is faster at 128: cfg4 0.325 vs 0.356 ms).
+// cfg3 0.129 -> 0.123 ms).  The NBG = 1 kernel: 80 registers (6 CTAs, 24 warps per SM)
+// measured cfg4 0.249 vs 0.257 ms at 128 (per-plan lanes), 0.227 ms with per-stage lanes.
 #ifndef CRIUS_EST_MINB_WIDE
 #define CRIUS_EST_MINB_WIDE 3
 #endif
@@ -1174,6 +1176,130 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
       }
     }
     __syncwarp();
+    // Per-stage lanes (below) or per-plan lanes (the loop after it), chosen per
+    // launch (A.per_stage): with few plans per unit the per-plan form leaves
+    // most lanes of a unit's one chunk idle while its longest plan runs S
+    // stages; with many, it packs plans by S and the per-stage form's
+    // reductions cost more than they save.  (Chosen per unit, warps of one SM
+    // run both forms and the kernel measured slower than either: DESIGN.md §5.)
+    if (A.per_stage && smax <= 32) {
+      // One (Cell, k, stage) per lane: a plan's S stages are S consecutive
+      // lanes.  Cells run by S descending (stable) and a Cell holds K*S items,
+      // so every plan's lane group is aligned to S inside one 32-lane chunk:
+      // xor butterflies of width S form its sum / max stage time and max sync
+      // (integer, so the reduction order is immaterial), the group's first
+      // lane holds the plan, and the segmented min-scan below picks the Cell's
+      // best plan as in the per-plan path.
+      for (int i = lane; i < nc; i += 32) {
+        const int si = CS[i];
+        int r = 0;
+        for (int q = 0; q < nc; ++q) r += CS[q] > si || (CS[q] == si && q < i);
+        ORD[r] = i;
+      }
+      __syncwarp();
+      {
+        int carry = 0;
+        for (int b0 = 0; b0 < nc; b0 += 32) {
+          const int r = b0 + lane;
+          int cnt = 0;
+          if (r < nc) {
+            const int ci = ORD[r];
+            cnt = (ilog2_pow2(CG[ci] / CS[ci]) + 1) * CS[ci];
+          }
+          const int inc = warp_incl_scan32(cnt, lane);
+          if (r < nc) CP[r + 1] = carry + inc;
+          carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) CP[0] = 0;
+      }
+      __syncwarp();
+      const int nitems = CP[nc];
+      int carry_r = -1, carry_p = 0;
+      int64_t carry_T = kInf;
+      for (int f0 = 0; f0 < nitems; f0 += 32) {
+        const int f = f0 + lane;
+        const bool valid = f < nitems;
+        int r = nc, p = 0, S = 1, s = 0, lB = 0;
+        bool bad = true;
+        int64_t Ts = 0, sy = 0;
+        if (valid) {
+          int lo = 0, hi = nc - 1;  // largest r with CP[r] <= f
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (CP[mid] <= f)
+              lo = mid;
+            else
+              hi = mid - 1;
+          }
+          r = lo;
+          const int ci = ORD[r], local = f - CP[r];
+          CRIUS_CHECK(ci >= 0 && ci < nc && local >= 0 && local < CP[r + 1] - CP[r]);
+          S = CS[ci];
+          const int lS = ilog2_pow2(S), lg = ilog2_pow2(CG[ci]) - lS;
+          p = local >> lS;
+          s = local & (S - 1);
+          lB = lS + 2;  // B = 4S (GPipe)
+          const int16_t *bd = BD + (S - 1) + lS;
+          int64_t Tc;
+          bad = !stage_terms(U, lg, p, lB, s, bd[s], bd[s + 1], Ts, Tc, sy);
+        }
+        const int Sw = __shfl_sync(0xffffffffu, S, 0);  // the chunk's largest S
+        int64_t sumT = Ts, maxT = Ts, maxSync = sy;
+        for (int d = 1; d < Sw; d <<= 1) {
+          const int64_t o1 = __shfl_xor_sync(0xffffffffu, sumT, d);
+          const int64_t o2 = __shfl_xor_sync(0xffffffffu, maxT, d);
+          const int64_t o3 = __shfl_xor_sync(0xffffffffu, maxSync, d);
+          if (d < S) {
+            sumT = (int64_t)((uint64_t)sumT + (uint64_t)o1);
+            maxT = max(maxT, o2);
+            maxSync = max(maxSync, o3);
+          }
+        }
+        const unsigned badm = __ballot_sync(0xffffffffu, bad);
+        const unsigned gmask = S == 32 ? 0xffffffffu : ((1u << S) - 1) << (lane & ~(S - 1));
+        int64_t T = kInf;
+        if (valid && s == 0 && !(badm & gmask))
+          T = (int64_t)((uint64_t)sumT + (uint64_t)((1ll << lB) - 1) * (uint64_t)maxT + (uint64_t)maxSync);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int64_t oT = __shfl_up_sync(0xffffffffu, T, d);
+          const int op = __shfl_up_sync(0xffffffffu, p, d);
+          const int orr = __shfl_up_sync(0xffffffffu, r, d);
+          if (lane >= d && orr == r && oT <= T) {
+            T = oT;
+            p = op;
+          }
+        }
+        const int next_r = __shfl_down_sync(0xffffffffu, r, 1);
+        const bool tail = valid && (lane == 31 || next_r != r);
+        if (tail && r == carry_r && carry_T <= T) {
+          T = carry_T;
+          p = carry_p;
+        }
+        const bool done = valid && (f + 1 == CP[r + 1]);
+        if (tail && done) {
+          CellResult res;
+          res.t_ns = T;
+          res.plan = T == kInf ? -1 : p;
+          res.flags = T == kInf ? 0 : 1;
+          emit_result(A, cb + ORD[r], out_cell_base, res);
+        }
+        const int r31 = __shfl_sync(0xffffffffu, r, 31);
+        const int64_t T31 = __shfl_sync(0xffffffffu, T, 31);
+        const int p31 = __shfl_sync(0xffffffffu, p, 31);
+        const bool open31 = __shfl_sync(0xffffffffu, (int)(valid && !done), 31);
+        if (open31) {
+          carry_r = r31;
+          carry_T = T31;
+          carry_p = p31;
+        } else {
+          carry_r = -1;
+          carry_T = kInf;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     // processing order: Cells by S descending (stable) so a 32-lane chunk runs
     // stage loops of one length; item = (Cell, k >= kmin, group of NBG microbatch counts)
     const bool sorted = npu / P.nB * ngrp > 32;  // one chunk: order does not matter

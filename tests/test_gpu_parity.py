@@ -127,6 +127,22 @@ def test_cfg4_all_pow2(crius, oracle_mod):
     assert_same(g, cells, t_ns, plan, rnd)
 
 
+@pytest.mark.parametrize("form", ["0", "1"])
+def test_plan_forms(crius, oracle_mod, monkeypatch, form):
+    """b_mode 0 evaluates plans either one per lane or one (plan, stage) per lane
+    with butterflies over aligned lane groups; the library picks per launch by
+    plans per unit (cfg4: per stage, the all-pow2 variant: per plan).
+    CRIUS_EST_PER_STAGE forces each form on the configs that default to the
+    other, and on small and tiny cases (ragged chunks, S up to 16)."""
+    monkeypatch.setenv("CRIUS_EST_PER_STAGE", form)
+    cases = [W.make_config(4, variant="pow2" if form == "1" else None), W.make_config(2)]
+    cases += [W.random_tiny(s, max_layers=12, n_types=3, n_jobs=6) for s in range(10)]
+    for pr in cases:
+        g = gpu_run(crius, pr, splits=True)
+        o, cells, t_ns, plan, rnd = oracle_run(oracle_mod, pr)
+        assert_same(g, cells, t_ns, plan, rnd)
+
+
 def test_cfg5_sampled_units(crius, oracle_mod):
     """Full-size cfg5 (96 layers, S <= 32, 7 B values): the GPU estimates every
     Cell; the oracle recomputes the Cells of 200 sampled units one by one."""
