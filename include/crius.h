@@ -341,8 +341,10 @@ crius_status crius_set_deadline_bounds(crius_ctx *ctx, const int64_t *t_max, voi
  * the admitted records lived in shared memory, [15] the round's bound on the
  * number of admitted records, [16..18] SM cycles of the per-type sequence
  * computations summed over types (preparation, moves, thresholds), [19]
- * candidate rescans, [20] type-list entries scanned, [26] SM cycles of the
- * commits' serial part, [28] CTA-wide barriers on the round's critical chain.
+ * candidate rescans, [20] type-list entries scanned, [21] top-list refills,
+ * [22] per-type sequence computations, [23] SM cycles of their top-list and
+ * cache refresh, [25] stale types summed over the recomputations, [28]
+ * CTA-wide barriers on the round's critical chain.
  * Other entries are reserved (0).  Synchronises `stream`. */
 crius_status crius_round_stats(crius_ctx *ctx, int64_t *out16, void *stream);
 

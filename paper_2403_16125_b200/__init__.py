@@ -407,6 +407,8 @@ class Crius:
                 11: "stale_caches", 12: "other_type_evals", 13: "seq_invalidations",
                 14: "records_in_smem", 15: "records_bound", 16: "seq_prep_cycles",
                 17: "seq_move_cycles", 18: "seq_tail_cycles", 19: "seq_rescans", 20: "seq_entries",
+                21: "top_refills", 22: "seq_type_runs", 23: "seq_top_refresh_cycles",
+                25: "seq_stale_types",
                 28: "cta_barriers"}
         return {k: int(out[i]) for i, k in keys.items()}
 

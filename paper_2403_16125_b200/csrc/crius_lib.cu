@@ -110,6 +110,7 @@ struct crius_ctx {
   int32_t *d_ao_pk = nullptr, *d_nao = nullptr, *d_rerr = nullptr, *d_ord = nullptr;
   double *d_ao_sc = nullptr, *d_osc = nullptr;
   uint64_t *d_gminb = nullptr, *d_tsb = nullptr;
+  uint8_t *d_operm = nullptr;
   AdmView adm_glob{};  // admitted-job records and type lists in global memory (beyond shared)
   int32_t round_policy = 0;  // crius_set_round_policy (NEXT-4 ablations)
   int64_t *d_tmax = nullptr;  // crius_set_deadline_bounds: [J] or unset
@@ -140,7 +141,7 @@ void free_all(crius_ctx *c) {
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
                   c->d_rng, c->d_cur, c->d_free, c->d_total, c->d_round_stats, c->d_score,
                   c->d_ao_pk, c->d_nao, c->d_rerr, c->d_ord, c->d_ao_sc, c->d_osc, c->d_gminb, c->d_tsb,
-                  c->adm_glob.bk, c->adm_glob.bl, c->adm_glob.ek, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
+                  c->d_operm, c->adm_glob.bk, c->adm_glob.bl, c->adm_glob.ek, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
                   c->adm_glob.t, c->adm_glob.slot, c->adm_glob.bi, c->adm_glob.ei, c->adm_glob.tl,
                   c->adm_glob.gmb, c->adm_glob.tsb, c->adm_glob.nopt, c->adm_glob.po,
                   c->d_run_opt, c->d_cand, c->d_run_cell, c->d_active};
@@ -955,6 +956,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
     CK(dalloc(&c->d_opt_cell, JO));
     CK(dalloc(&c->d_ao_pk, JO));
     CK(dalloc(&c->d_ao_sc, JO));
+    CK(dalloc(&c->d_operm, JO));
     CK(dalloc(&c->d_ref, J));
     CK(dalloc(&c->d_decision, J));
     CK(dalloc(&c->d_nopt, J));
@@ -1029,6 +1031,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   R.nao = c->d_nao;
   R.gminb = c->d_gminb;
   R.tsb = c->d_tsb;
+  R.operm = c->d_operm;
   R.run_cell = run_cell ? c->d_run_cell : nullptr;
   R.active = active ? c->d_active : nullptr;
   R.run_opt = c->d_run_opt;

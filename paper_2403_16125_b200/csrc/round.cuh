@@ -66,7 +66,7 @@ struct AdmView {
   int32_t *po;  // offset of the job's options in the shared-memory pool, -1 = not staged
   int32_t *tl;  // per-type lists of admitted records, type u at tl + toff[u]
   double *psc;  // option pool (shared memory): scores
-  int32_t *ppk; //   and log2 G | t << 8
+  int32_t *ppk; //   and log2 G | t << 8 | (index of the entry's rank in score order) << 16
 };
 
 struct RoundBuf {
@@ -94,6 +94,8 @@ struct RoundBuf {
   int32_t *nao;          // [J] by position
   uint64_t *gminb;       // [J] byte u = log2 of the job's smallest option G on type u (0xff none)
   uint64_t *tsb;         // [J] byte u = index of the job's first option on type u
+  uint8_t *operm;        // [J][maxopt] by position: option indices by score descending
+                         // (equal scores: lower index first)
   // NEXT-4 round state (NULL = every job active, none running)
   const int64_t *run_cell;  // [J] by job: Cell the job runs on, or -1
   const uint8_t *active;    // [J] by job: the job takes part in this round
@@ -172,6 +174,8 @@ __device__ __forceinline__ void round_options_job(const Params &P, const int64_t
   }
   const int64_t ref = ref_ng != kInf ? ref_ng : ref_any;
   double *sc = R.score + (int64_t)pos * R.maxopt;
+  double sl[kLocal ? kLocalOpt : 1];
+  double *scw = kLocal ? sl : sc;
   uint64_t gmb = ~0ull, tsv = ~0ull;
   for (int i = 0; i < n; ++i) {
     const OptRec x = o[i];
@@ -179,7 +183,9 @@ __device__ __forceinline__ void round_options_job(const Params &P, const int64_t
       og[i] = x;
       ocg[i] = oc[i];
     }
-    sc[i] = score_of(ref, x.T);
+    const double si = score_of(ref, x.T);
+    sc[i] = si;
+    if (kLocal) sl[i] = si;
     const int sh = 8 * x.t;
     if (((gmb >> sh) & 0xff) == 0xff) {  // first (smallest G) option of its type
       gmb = (gmb & ~(0xffull << sh)) | ((uint64_t)ilog2_pow2((uint32_t)x.G) << sh);
@@ -188,6 +194,14 @@ __device__ __forceinline__ void round_options_job(const Params &P, const int64_t
   }
   R.gminb[pos] = gmb;
   R.tsb[pos] = tsv;
+  // options by score descending (the order of loss = score(cur) - score(o'))
+  uint8_t *pm = R.operm + (int64_t)pos * R.maxopt;
+  for (int i = 0; i < n; ++i) {
+    const double si = scw[i];
+    int r = 0;
+    for (int i2 = 0; i2 < n; ++i2) r += scw[i2] > si || (scw[i2] == si && i2 < i);
+    pm[r] = (uint8_t)i;
+  }
   // arrival options (G <= N_G) in kappa order: rank by counting
   int na = 0;
   for (int i = 0; i < n; ++i) {
@@ -291,6 +305,7 @@ struct SeqTab {
   uint64_t gq;  // byte u <= log2 of the smallest option G on type u over the type's jobs (a lower
                 // bound: records only join a type's bound, never leave it -- conservative)
   uint32_t iit;  // types that the sequence's other-type moves go to
+  uint32_t plim_lo, plim_hi;  // the fit limits (lim bytes) at the last computation's start
   // top list: the tcnt smallest same-type (case i) candidates of the type's
   // jobs, ascending by (key, priority, option); tall = it holds all of them
   double tk[kTop], tlo[kTop];
@@ -319,7 +334,7 @@ struct RoundShared {
   int32_t bs_nopt[kRoundThreads];
   int32_t wsum[kRoundWarps];
   long long prof[8], prof2[8];
-  int32_t cnt[8];
+  int32_t cnt[12];
 };
 
 // ---- type lists -------------------------------------------------------------
@@ -346,7 +361,7 @@ __device__ __forceinline__ void opt_get(const RoundBuf &R, const AdmView &A, int
   if (po >= 0) {
     const int pk = A.ppk[po + i];
     lg = pk & 0xff;
-    t = pk >> 8;
+    t = (pk >> 8) & 0xff;
     s = A.psc[po + i];
   } else {
     const OptRec o = ldg_opt(R.opt + (int64_t)p * R.maxopt + i);
@@ -396,9 +411,13 @@ __device__ __forceinline__ void refresh_i(const RoundBuf &R, const AdmView &A, i
 // One lane: the job's best other-type move (case ii) under free' = f2: argmin
 // over its options on other types with G2 <= f2[t2] of loss = score(cur) -
 // score(o'), ties -> lowest index; key = loss / G_cur (exact: G_cur is a power
-// of two).  Returns the packed move or -1.
+// of two).  Returns the packed move or -1.  At a sequence's start (free' = the
+// state's free counts) the cached move is tagged kEiStart: it stays the argmin
+// while the job's option is unchanged and no type's free count gains a power-of-
+// two level (the options that fit only shrink) as long as it still fits itself.
+constexpr int kEiStart = 1 << 30;
 __device__ __forceinline__ int compute_ii(const RoundBuf &R, const AdmView &A, int a,
-                                          const int32_t *f2) {
+                                          const int32_t *f2, bool at_start = false) {
   const int p = A.pos[a], cv = A.cur[a], tt = A.t[a], Gc = A.G[a], po = A.po[a];
   const int nv = A.nopt[a];
   int lg, t2;
@@ -406,19 +425,46 @@ __device__ __forceinline__ int compute_ii(const RoundBuf &R, const AdmView &A, i
   opt_get(R, A, po, p, cv, lg, t2, sc);
   int bi = -1;
   double bl = 0.0;
-#pragma unroll 4
-  for (int i2 = 0; i2 < nv; ++i2) {
-    double s2;
-    opt_get(R, A, po, p, i2, lg, t2, s2);
-    if (t2 == tt || (1 << lg) > f2[t2]) continue;
-    const double l = __dsub_rn(sc, s2);
-    if (bi < 0 || l < bl) {
-      bi = i2 | (lg << 8) | (t2 << 16);
-      bl = l;
+  // options by score descending: loss = RN(score(cur) - score(o')) is
+  // nondecreasing along them, so the first one that fits has the least loss;
+  // later ones of equal loss (rounding) may have a lower index
+  // (four entries per step: their loads are independent and issue together)
+  const uint8_t *pm = R.operm + (int64_t)p * R.maxopt;
+  constexpr int kW = 4;
+  for (int r0 = 0; r0 < nv; r0 += kW) {
+    int iv[kW], pv[kW];
+    double sv[kW];
+    bool ok[kW];
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      const int r = min(r0 + q, nv - 1);
+      iv[q] = po >= 0 ? (A.ppk[po + r] >> 16) & 0xff : (int)__ldg(pm + r);
     }
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      int lq, tq;
+      opt_get(R, A, po, p, iv[q], lq, tq, sv[q]);
+      pv[q] = iv[q] | (lq << 8) | (tq << 16);
+      ok[q] = r0 + q < nv && tq != tt && (1 << lq) <= f2[tq];
+    }
+    bool stop = false;
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      if (stop || !ok[q]) continue;
+      const double l = __dsub_rn(sc, sv[q]);
+      if (bi >= 0 && l != bl) {
+        stop = true;
+      } else if (bi < 0 || iv[q] < (bi & 0xff)) {
+        bi = pv[q];
+        bl = l;
+      }
+    }
+    if (stop) break;
   }
-  A.ei[a] = bi;
-  if (bi >= 0) A.ek[a] = __ddiv_rn(bl, (double)Gc);
+  A.ei[a] = bi >= 0 && at_start ? bi | kEiStart : bi;
+  // bl / G_cur: G_cur = 2^k, so the quotient is the product with 2^-k (the
+  // same real value, rounded once either way)
+  if (bi >= 0) A.ek[a] = __dmul_rn(bl, __longlong_as_double((long long)(1023 - ilog2_pow2((uint32_t)Gc)) << 52));
   return bi;
 }
 
@@ -449,7 +495,7 @@ __device__ __forceinline__ Cand ii_cand(const AdmView &A, int a, int ei) {
     c.key = A.ek[a];
     c.tie = ((uint32_t)A.pos[a] << 8) | (ei & 0xff);
     c.a = a;
-    c.pk = ei;
+    c.pk = ei & ~kEiStart;
   }
   return c;
 }
@@ -585,6 +631,9 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     lim_lo = __reduce_or_sync(0xffffffffu, sl);
     lim_hi = __reduce_or_sync(0xffffffffu, sh_);
   }
+  // no type's limit grew since the last computation: cached start moves that
+  // still fit stay exact (compute_ii)
+  const bool mono = (__vcmpgtu4(lim_lo, S.plim_lo) | __vcmpgtu4(lim_hi, S.plim_hi)) == 0;
   // ---- (1) the top list: drop entries whose record changed or left the type
   int cnt = S.tcnt;
   bool all = S.tall != 0;
@@ -660,20 +709,35 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
         listed = (__vcmpltu4((uint32_t)gb, lim_lo) | __vcmpltu4((uint32_t)(gb >> 32), lim_hi)) != 0;
         if (!listed) A.ei[a] = -1;
       }
+      bool fresh = false;  // listed with an exact cached start move
+      if (listed && mono) {
+        const int ei = A.ei[a];
+        fresh = ei >= 0 && (ei & kEiStart) && ii_fits(ei, f2);
+      }
       const uint32_t ml = __ballot_sync(0xffffffffu, listed);
       const int slot = nl + __popc(ml & ((1u << lane) - 1));
-      if (listed && slot < kQ) ql[slot] = a;
+      if (listed && slot < kQ) ql[slot] = fresh ? ~a : a;
       nl += __popc(ml);
-      if (listed && slot >= kQ) {  // queue full: evaluate this one in place
-        compute_ii(R, A, a, f2);
+      if (listed && slot >= kQ && !fresh) {  // queue full: evaluate this one in place
+        compute_ii(R, A, a, f2, true);
+        ++n_ii;
       }
     }
     __syncwarp();
-    n_ii = nl;
     own_tl = nl > kQ;
     const int nq = min(nl, kQ);
-    for (int i = lane; i < nq; i += 32) compute_ii(R, A, ql[i], f2);
+    for (int i = lane; i < nq; i += 32) {
+      const int qa = ql[i];
+      if (qa >= 0) {
+        compute_ii(R, A, qa, f2, true);
+        ++n_ii;
+      } else {
+        ql[i] = ~qa;
+      }
+    }
+    n_ii = __reduce_add_sync(0xffffffffu, n_ii);
     __syncwarp();
+
     if (!own_tl) {
       for (int i = lane; i < nq; i += 32) {
         const int a = ql[i];
@@ -700,14 +764,22 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   bool imov = false;  // this lane's top-list entry was moved
   int m = 0, n_rescan = 0;
   double cacc = 0.0;  // ((0 + loss_1) + loss_2) + ... (fp64, in move order as in the oracle)
+  // the lanes' best other-type candidate (argmin over b1), kept while no
+  // lane's b1 changes (a same-type move that no other-type entry refers to)
+  int src = -1;
+  double sk = 0.0;
+  uint32_t st = 0;
+  bool b1_dirty = true;
   for (; m < R.depth; ++m) {
     const uint32_t im = __ballot_sync(0xffffffffu, lane < cnt && !imov);
     const int h = im ? __ffs(im) - 1 : 0;
     const double hk = __shfl_sync(0xffffffffu, x.k, h);
     const uint32_t ht = __shfl_sync(0xffffffffu, x.tie, h);
-    const int src = warp_lex_argmin(b1.have, ord_double(b1.have ? b1.key : 0.0), b1.tie);
-    const double sk = __shfl_sync(0xffffffffu, b1.key, max(src, 0));
-    const uint32_t st = __shfl_sync(0xffffffffu, b1.tie, max(src, 0));
+    if (b1_dirty) {
+      src = warp_lex_argmin(b1.have, ord_double(b1.have ? b1.key : 0.0), b1.tie);
+      sk = __shfl_sync(0xffffffffu, b1.key, max(src, 0));
+      st = __shfl_sync(0xffffffffu, b1.tie, max(src, 0));
+    }
     int wa, wpk;
     bool wii;
     double wl;
@@ -738,7 +810,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     __syncwarp();
     if (lane < TT) S.dfr[m + 1][lane] = f2[lane] - sh.fr[lane];
     if (lane < cnt && x.a == wa) imov = true;
-    bool rs = false;
+    bool rs = false, b1_ch = false;
     if (b2.have && b2.a == wa) {  // the moved job's other-type entry leaves the lane's pair
       b2.have = false;
       b2_known = false;
@@ -748,6 +820,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
       b2.have = false;
       rs = !b2_known;
       b2_known = false;
+      b1_ch = true;
     }
     if (wii) {  // an other-type move only shrinks free' of type t2
       if (b1.have && !ii_fits(b1.pk, f2)) rs = true;
@@ -771,7 +844,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
         top2_take(b1, b2, ii_cand(A, a, ei));
       }
     }
-    __syncwarp();
+    b1_dirty = __any_sync(0xffffffffu, b1_ch || rs);
   }
   n_rescan = __reduce_add_sync(0xffffffffu, n_rescan);
   if (lane == 0) atomicAdd(&sh.cnt[3], n_rescan);
@@ -789,6 +862,8 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
   if (lane == 0) {
     S.cum[0] = 0.0;
     S.len = m;
+    S.plim_lo = lim_lo;
+    S.plim_hi = lim_hi;
     S.iit = iit;
   }
   __syncwarp();
@@ -812,6 +887,7 @@ __device__ void type_sequence(RoundShared &sh, const RoundBuf &R, const AdmView 
     atomicAdd((unsigned long long *)&sh.prof[4], (unsigned long long)(c2 - c1));
     atomicAdd((unsigned long long *)&sh.prof[5], (unsigned long long)(c3 - c2));
     atomicAdd((unsigned long long *)&sh.prof2[0], (unsigned long long)(ca - c0));
+    atomicAdd(&sh.cnt[6], 1);
   }
 }
 
@@ -882,6 +958,7 @@ __device__ __forceinline__ void adm_point(RoundShared &sh, const AdmView &A, int
   A.G[a] = G;
   A.t[a] = t;
   A.bi[a] = -2;
+  A.ei[a] = -1;
   sh.vic[sh.n_vic++] = a;
 }
 // po: the record's pool offset (allocated by the caller), -1 = none
@@ -936,7 +1013,8 @@ __device__ __forceinline__ void stage_options(const RoundBuf &R, const AdmView &
     const int p = A.pos[a], nv = A.nopt[a];
     for (int i = lane & 15; i < nv; i += 16) {
       const OptRec o = ldg_opt(R.opt + (int64_t)p * R.maxopt + i);
-      A.ppk[po + i] = ilog2_pow2((uint32_t)o.G) | (o.t << 8);
+      A.ppk[po + i] = ilog2_pow2((uint32_t)o.G) | (o.t << 8) |
+                      ((int)__ldg(R.operm + (int64_t)p * R.maxopt + i) << 16);
       A.psc[po + i] = __ldg(R.score + (int64_t)p * R.maxopt + i);
     }
   }
@@ -947,7 +1025,8 @@ __device__ __forceinline__ void stage_job(const RoundBuf &R, const AdmView &A, i
   const int lane = threadIdx.x & 31;
   for (int i = lane; i < nv; i += 32) {
     const OptRec o = ldg_opt(R.opt + (int64_t)pos * R.maxopt + i);
-    A.ppk[po + i] = ilog2_pow2((uint32_t)o.G) | (o.t << 8);
+    A.ppk[po + i] = ilog2_pow2((uint32_t)o.G) | (o.t << 8) |
+                    ((int)__ldg(R.operm + (int64_t)pos * R.maxopt + i) << 16);
     A.psc[po + i] = __ldg(R.score + (int64_t)pos * R.maxopt + i);
   }
 }
@@ -975,6 +1054,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
     sh.prof[tid] = 0;
     sh.prof2[tid] = 0;
     sh.cnt[tid] = 0;
+    if (tid < 4) sh.cnt[8 + tid] = 0;
   }
   if (tid == 0) {
     sh.n_adm = 0;
@@ -986,6 +1066,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
     sh.sq[tid].tcnt = 0;
     sh.sq[tid].tall = 1;
     sh.sq[tid].gq = ~0ull;
+    sh.sq[tid].plim_lo = sh.sq[tid].plim_hi = 0u;
   }
   __syncthreads();
   long long c_start = clock64();
@@ -1209,6 +1290,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       if (nb) {
         if (sh.stale) {
           const long long c0 = clock64();
+          if (tid == 0) sh.cnt[7] += __popc(sh.stale);
           if (wid < TT && ((sh.stale >> wid) & 1)) type_sequence(sh, R, A, wid);
           __syncthreads();
       ++n_bar;
@@ -1329,6 +1411,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
               moved_type = ((pk >> 16) & 0xff) != t;
               A.cur[a] = pk & 0xff;
               A.G[a] = 1 << ((pk >> 8) & 0xff);  // bi: warp 3 writes the refreshed cache
+              A.ei[a] = -1;
               sh.vic[sh.n_vic + lane] = a;
             }
             const uint32_t mt = __ballot_sync(0xffffffffu, moved_type);
@@ -1470,6 +1553,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
             list_add(sh, A, aa, x.t);
           }
           A.cur[aa] = sh.res[f];
+          A.ei[aa] = -1;
           A.G[aa] = x.G;
           A.t[aa] = x.t;
           sh.fr[x.t] -= x.G;
@@ -1519,6 +1603,11 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       R.stats[18] = sh.prof[5];
       R.stats[19] = sh.cnt[3];
       R.stats[20] = sh.cnt[4];
+      R.stats[21] = sh.cnt[5];
+      R.stats[22] = sh.cnt[6];
+      R.stats[23] = sh.prof2[0];
+      R.stats[25] = sh.cnt[7];
+
       R.stats[28] = n_bar;
     }
   }
