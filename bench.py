@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--variant", default=None)
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=4,
+                    help="N=1 e2e: crius_update_estimate with the row upload pipelined in this "
+                         "many job ranges (0: update + enumerate + estimate, unpipelined)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--json-out", default=None)
@@ -502,6 +505,9 @@ def main():
                 assert pl.job_range(rank, pr.n_types) == (j0, j1)
                 res = (xch.estimate_all(pl) if xch is not None else
                        sharded.estimate_all(cr, pl, rank, mine=mine, gathered=gathered, full=full))
+            elif a.e2e_chunks > 0:
+                # one call: rows uploaded in chunks, each estimated once resident
+                res = cr.update_estimate(pr, chunks=a.e2e_chunks, out=mine)
             else:
                 cr.update(pr)
                 cr.enumerate()
@@ -528,7 +534,10 @@ def main():
             dist.all_reduce(bytes_t)  # whole-job bytes: every rank's copies
         e2e = {"value": n_plans / (e2e_ms / 1e3), "unit": "cell-plans/s",
                "h2d_bytes_per_step": int(bytes_t[0]), "d2h_bytes_per_step": int(bytes_t[1]),
-               "ms_per_step": e2e_ms}
+               "ms_per_step": e2e_ms,
+               "path": ("crius_update_estimate, rows in %d pipelined chunks + round" % a.e2e_chunks
+                        if world == 1 and a.e2e_chunks > 0 else
+                        "update + enumerate + estimate (+ gather) + round")}
 
     rstats = cr.round_stats()
     sm_mhz = float(clocks.get("sm_mhz") or 1965.0)

@@ -172,6 +172,29 @@ crius_status crius_partition_units(crius_ctx *ctx, int32_t world, int64_t *unit_
 crius_status crius_estimate_cells(crius_ctx *ctx, int64_t unit_begin, int64_t unit_end,
                                   crius_cell_result *d_out, int16_t *d_splits, void *stream);
 
+/* One call per new batch of profiles (the same shapes as loaded): the effect of
+ * crius_update_profiles + crius_enumerate_cells + crius_estimate_cells over
+ * every unit, with the per-layer row upload (the bulk of the input bytes)
+ * pipelined against the work that needs it.  The per-job arrays go up on
+ * `stream` and the Cells are enumerated from them while the rows go up in
+ * n_chunks (1..64) job ranges of equal layer count on a stream of the context;
+ * each range's rows are bound-checked and its units estimated on `stream` as
+ * soon as they are resident.  Host arrays as crius_update_profiles (pinned host
+ * memory lets the copies overlap; pageable memory still works, without
+ * overlap).  d_out: caller-owned DEVICE buffer of out_capacity records; record
+ * of Cell i at d_out[i] (GLOBAL Cell order); d_splits (optional DEVICE buffer
+ * of n_units * crius_split_stride entries) at unit u's row u * stride.
+ * Synchronises `stream`; returns the counts as crius_enumerate_cells (also on
+ * failure once enumerated).  EINVAL as crius_update_profiles (the records are
+ * then not valid and the context needs a new enumeration) or when n_cells >
+ * out_capacity (nothing estimated: grow d_out to the returned n_cells and call
+ * again); EINFEASIBLE if 0 Cells.  The default single-GPU estimator only. */
+crius_status crius_update_estimate(crius_ctx *ctx, const crius_cluster *cluster,
+                                   const crius_jobs *jobs, int32_t n_chunks,
+                                   crius_cell_result *d_out, int64_t out_capacity,
+                                   int16_t *d_splits, int64_t *n_cells, int64_t *n_cell_plans,
+                                   int64_t *n_units, void *stream);
+
 /* NEXT-1: per-stage parallelism assembly -- the paper's own
  * sampling, where each stage picks its parallelism independently ("assemble
  * 2^{N_S} distinct parallelism plans") -- with either pipeline

@@ -72,7 +72,7 @@ class _CellView(C.Structure):
 EXPORTS = ["crius_load_profiles", "crius_update_profiles", "crius_update_profiles_range",
            "crius_enumerate_cells", "crius_cells",
            "crius_split_stride", "crius_max_stages", "crius_partition_units",
-           "crius_estimate_cells", "crius_estimate_assembled", "crius_tune_assembled",
+           "crius_estimate_cells", "crius_update_estimate", "crius_estimate_assembled", "crius_tune_assembled",
            "crius_estimate_paper_stages",
            "crius_compact_gathered", "crius_exchange_init", "crius_exchange_open",
            "crius_estimate_exchange", "crius_exchange_wait", "crius_exchange_close",
@@ -104,6 +104,8 @@ def lib():
         L.crius_split_stride.restype = i32
         L.crius_partition_units.argtypes = [vp, i32, vp, vp, vp]
         L.crius_estimate_cells.argtypes = [vp, i64, i64, vp, vp, vp]
+        L.crius_update_estimate.argtypes = [vp, C.POINTER(_Cluster), C.POINTER(_Jobs), i32, vp, i64,
+                                            vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), vp]
         L.crius_estimate_assembled.argtypes = [vp, C.POINTER(_Assembly), i64, i64, vp, vp, vp]
         L.crius_tune_assembled.argtypes = [vp, i32, i64, i64, vp, vp, vp, vp]
         L.crius_estimate_paper_stages.argtypes = [vp, i64, i64, vp, vp, vp, vp]
@@ -260,6 +262,32 @@ class Crius:
         sp = C.c_void_p(splits.data_ptr()) if splits is not None else None
         _check(lib().crius_estimate_cells(self.ctx, int(unit_begin), int(unit_end),
                                           C.c_void_p(out.data_ptr()), sp, _stream_handle(stream)))
+        return out
+
+    def update_estimate(self, pr, chunks=4, out=None, splits=None, stream=None):
+        """New profile values from host memory -> every Cell's record, with the
+        per-layer row upload pipelined against the estimate in `chunks` job
+        ranges (crius_update_estimate; pinned host arrays overlap).  Returns the
+        [n_cells, 2] records (global Cell order)."""
+        cl, jb, _ = self._structs(pr)
+        if out is None:
+            if self.n_cells is None:
+                self.enumerate(stream)
+            out = self.new_results(self.n_cells)
+        n, p, u = C.c_int64(), C.c_int64(), C.c_int64()
+        sp = C.c_void_p(splits.data_ptr()) if splits is not None else None
+        st = lib().crius_update_estimate(self.ctx, C.byref(cl), C.byref(jb), int(chunks),
+                                         C.c_void_p(out.data_ptr()), int(out.shape[0]), sp,
+                                         C.byref(n), C.byref(p), C.byref(u), _stream_handle(stream))
+        if st == 2 and n.value > out.shape[0]:  # more Cells than `out` holds: grow, call again
+            out = self.new_results(n.value)
+            st = lib().crius_update_estimate(self.ctx, C.byref(cl), C.byref(jb), int(chunks),
+                                             C.c_void_p(out.data_ptr()), int(out.shape[0]), sp,
+                                             C.byref(n), C.byref(p), C.byref(u),
+                                             _stream_handle(stream))
+        _check(st)
+        self.pr = pr
+        self.n_cells, self.n_plans, self.n_units = n.value, p.value, u.value
         return out
 
     def max_stages(self):

@@ -111,6 +111,10 @@ struct crius_ctx {
   double *d_ao_sc = nullptr, *d_osc = nullptr;
   uint64_t *d_gminb = nullptr, *d_tsb = nullptr;
   uint8_t *d_operm = nullptr;
+  // crius_update_estimate: the row upload runs on its own stream, one event per chunk
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
   AdmView adm_glob{};  // admitted-job records and type lists in global memory (beyond shared)
   int32_t round_policy = 0;  // crius_set_round_policy (NEXT-4 ablations)
   int64_t *d_tmax = nullptr;  // crius_set_deadline_bounds: [J] or unset
@@ -130,6 +134,8 @@ struct crius_ctx {
 };
 
 namespace {
+
+constexpr int kMaxChunks = 64;  // crius_update_estimate row chunks
 
 void free_all(crius_ctx *c) {
   void *ptrs[] = {c->d_ng, c->d_gb, c->d_kst, c->d_L, c->d_off, c->d_submit, c->d_id, c->d_c,
@@ -218,10 +224,10 @@ crius_status validate_static(const crius_cluster *cl, const crius_jobs *jb, cons
   return CRIUS_OK;
 }
 
+crius_status copy_rows(crius_ctx *c, const crius_jobs *jb, int T, cudaStream_t st, int j0, int j1);
 crius_status copy_inputs(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
                          cudaStream_t st, int j0, int j1) {
   const int J = jb->n_jobs, T = cl->n_types;
-  const size_t TL = (size_t)c->TL;
   CK(cudaMemcpyAsync(c->d_ng, jb->n_gpus_req, J * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->d_gb, jb->global_batch, J * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->d_kst, jb->k_state, J * 4, cudaMemcpyHostToDevice, st));
@@ -229,8 +235,13 @@ crius_status copy_inputs(crius_ctx *c, const crius_cluster *cl, const crius_jobs
   CK(cudaMemcpyAsync(c->d_off, jb->layer_off, (J + 1) * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->d_submit, jb->submit_time, J * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->d_id, jb->job_id, J * 8, cudaMemcpyHostToDevice, st));
+  return copy_rows(c, jb, T, st, j0, j1);
+}
+
+// Per-layer rows of jobs [j0, j1): layers [l0, l1), one strided 2-D copy for c.
+crius_status copy_rows(crius_ctx *c, const crius_jobs *jb, int T, cudaStream_t st, int j0, int j1) {
   if (j1 <= j0) return CRIUS_OK;
-  // per-layer rows of jobs [j0, j1): layers [l0, l1), one strided 2-D copy for c
+  const size_t TL = (size_t)c->TL;
   const size_t l0 = (size_t)jb->layer_off[j0], nl = (size_t)jb->layer_off[j1] - l0;
   const size_t planes = (size_t)T * (jb->k_max + 1);
   if (nl == TL) {
@@ -262,13 +273,16 @@ void fill_types(crius_ctx *c, const crius_cluster *cl) {
   }
 }
 
-// Device stats of c -> §N0 bounds; then priority ranks.  Synchronises.
-crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
-                         const crius_config *cf, cudaStream_t st, int j0, int j1) {
-  const int J = jb->n_jobs;
+// Scratch for the checks: per-job status words and the smallest compute value.
+crius_status check_init(crius_ctx *c, int J, cudaStream_t st) {
   CK(cudaMemsetAsync(c->d_scratch, 0, (J + 8) * 4, st));
-  int32_t big = INT32_MAX;
+  static const int32_t big = INT32_MAX;
   CK(cudaMemcpyAsync(c->d_scratch + J, &big, 4, cudaMemcpyHostToDevice, st));
+  return CRIUS_OK;
+}
+// Device bound checks of the rows of jobs [j0, j1) (per-job status in scratch).
+crius_status check_rows(crius_ctx *c, const crius_cluster *cl, const crius_config *cf, int J,
+                        cudaStream_t st, int j0, int j1) {
   if (j1 > j0) {
     BoundArgs BA{};
     for (int t = 0; t < cl->n_types; ++t) {
@@ -280,7 +294,13 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
     BA.bmax_list = cf->b_mode == 1 ? cf->b_values[cf->b_count - 1] : 0;
     k_profile_check<<<j1 - j0, 64, 0, st>>>(c->P, j0, BA, c->d_scratch, c->d_scratch + J);
     CKL();
+    c->launches += 1;
   }
+  return CRIUS_OK;
+}
+// Priority order pi (launches only when submit/id changed).
+crius_status sort_priority(crius_ctx *c, const crius_jobs *jb, cudaStream_t st) {
+  const int J = jb->n_jobs;
   // priority order pi by (submit, id) (A-18): recomputed only when they changed
   const bool same = c->h_submit.size() == (size_t)J &&
                     std::equal(c->h_submit.begin(), c->h_submit.end(), jb->submit_time) &&
@@ -306,7 +326,11 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
     k_priority_scatter<<<(unsigned)((J + 255) / 256), 256, 0, st>>>(ja, J, c->d_pi, c->d_rank);
     CKL();
   }
-  c->launches += n_sort + (j1 > j0);
+  c->launches += n_sort;
+  return CRIUS_OK;
+}
+// The checks' verdict (synchronises).
+crius_status check_result(crius_ctx *c, int J, cudaStream_t st, int j0, int j1) {
   std::vector<int32_t> stats(J + 1);
   CK(cudaMemcpyAsync(stats.data(), c->d_scratch, (J + 1) * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -318,6 +342,17 @@ crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs
     if (stats[j] != 0)
       return fail(CRIUS_EINVAL, "job " + std::to_string(j) + ": " + why[std::min(stats[j], 5)]);
   return CRIUS_OK;
+}
+
+// Device stats of c -> §N0 bounds; then priority ranks.  Synchronises.
+crius_status finish_load(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
+                         const crius_config *cf, cudaStream_t st, int j0, int j1) {
+  const int J = jb->n_jobs;
+  crius_status s = check_init(c, J, st);
+  if (s == CRIUS_OK) s = check_rows(c, cl, cf, J, st, j0, j1);
+  if (s == CRIUS_OK) s = sort_priority(c, jb, st);
+  if (s == CRIUS_OK) s = check_result(c, J, st, j0, j1);
+  return s;
 }
 
 }  // namespace
@@ -636,7 +671,7 @@ constexpr int64_t kXchCapOff = 128;  // ... and the window's capacity (int64)
 crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_begin,
                              int64_t unit_end, crius_cell_result *d_out, int16_t *d_splits,
                              int8_t *d_stage_tp, const int8_t *d_favor, cudaStream_t st,
-                             bool exchange = false) {
+                             bool exchange = false, bool global_out = false) {
   if (!c->enumerated) return fail(CRIUS_ESTATE, "estimate before enumerate");
   if (unit_begin < 0 || unit_end > c->n_units || unit_begin > unit_end)
     return fail(CRIUS_EINVAL, "bad unit range");
@@ -674,6 +709,7 @@ crius_status launch_estimate(crius_ctx *c, int amode, int form, int64_t unit_beg
   A.unit_end = unit_end;
   A.out = (CellResult *)d_out;
   A.splits = d_splits;
+  A.global_out = global_out;
   A.split_stride = crius_split_stride(c);
   A.work_counter = c->d_counter;
   A.form = form;
@@ -771,6 +807,100 @@ crius_status crius_estimate_cells(crius_ctx *c, int64_t unit_begin, int64_t unit
   if (!c) return fail(CRIUS_EINVAL, "null ctx");
   return launch_estimate(c, 0, 0, unit_begin, unit_end, d_out, d_splits, nullptr, nullptr,
                          (cudaStream_t)stream);
+}
+
+crius_status crius_update_estimate(crius_ctx *c, const crius_cluster *cl, const crius_jobs *jb,
+                                   int32_t n_chunks, crius_cell_result *d_out, int64_t out_capacity,
+                                   int16_t *d_splits, int64_t *n_cells, int64_t *n_cell_plans,
+                                   int64_t *n_units, void *stream) {
+  CRIUS_ABI_RANGE();
+  if (!c) return fail(CRIUS_EINVAL, "null ctx");
+  if (!d_out) return fail(CRIUS_EINVAL, "null d_out");
+  if (n_chunks < 1 || n_chunks > kMaxChunks)
+    return fail(CRIUS_EINVAL, "update_estimate: n_chunks outside [1, 64]");
+  if (!cl || !jb || cl->n_types != c->P.T || jb->n_jobs != c->P.J || jb->k_max != c->k_max)
+    return fail(CRIUS_EINVAL, "update_profiles: shape differs from the loaded problem");
+  crius_config cf{};
+  cf.gpu_set = c->P.gpu_set;
+  cf.s_max = c->P.s_max;
+  cf.g_max = c->P.g_max;
+  cf.b_mode = c->P.b_mode;
+  std::vector<int32_t> bv;
+  for (int b = 0; b < (c->P.b_mode ? c->P.nB : 0); ++b) bv.push_back(1 << c->P.lB[b]);
+  cf.b_count = (int32_t)bv.size();
+  cf.b_values = bv.data();
+  cf.search_depth = c->P.depth;
+  int64_t TL = 0;
+  int32_t Lmax = 0;
+  crius_status s = validate_static(cl, jb, &cf, &TL, &Lmax);
+  if (s != CRIUS_OK) return s;
+  if (TL != c->TL) return fail(CRIUS_EINVAL, "update_profiles: total layers differ");
+  for (int t = 0; t < cl->n_types; ++t)
+    if (cl->capacity[t] != c->cap[t]) return fail(CRIUS_EINVAL, "update_profiles: capacity differs");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int J = c->P.J, T = c->P.T;
+  n_chunks = std::min(n_chunks, J);
+  if (!c->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+    c->ev_chunk.resize(kMaxChunks);
+    for (cudaEvent_t &e : c->ev_chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  fill_types(c, cl);
+  c->Lmax = Lmax;
+  c->enumerated = false;
+  // per-job arrays on `stream`; the rows on the copy stream, which first waits
+  // for the work already queued on `stream` (it may still read the old rows)
+  s = copy_inputs(c, cl, jb, st, 0, 0);
+  if (s != CRIUS_OK) return s;
+  CK(cudaEventRecord(c->ev_start, st));
+  CK(cudaStreamWaitEvent(c->copy_stream, c->ev_start, 0));
+  // chunk q = jobs [jq[q], jq[q+1]), cut at equal layer counts (equal bytes)
+  std::vector<int> jq(n_chunks + 1, J);
+  jq[0] = 0;
+  for (int q = 1, j = 0; q < n_chunks; ++q) {
+    const int64_t want = TL * q / n_chunks;
+    while (j < J && jb->layer_off[j] < want) ++j;
+    jq[q] = std::max(jq[q - 1], j);
+  }
+  // on any failure from here the caller's host rows must outlive the copies
+  auto bail = [&](crius_status e) {
+    cudaStreamSynchronize(c->copy_stream);
+    return e;
+  };
+  for (int q = 0; q < n_chunks; ++q) {
+    s = copy_rows(c, jb, T, c->copy_stream, jq[q], jq[q + 1]);
+    if (s != CRIUS_OK) return bail(s);
+    CK(cudaEventRecord(c->ev_chunk[q], c->copy_stream));
+  }
+  c->rows_j0 = 0;
+  c->rows_j1 = J;
+  s = check_init(c, J, st);
+  if (s == CRIUS_OK) s = sort_priority(c, jb, st);
+  if (s != CRIUS_OK) return bail(s);
+  // enumeration needs only the per-job arrays: it runs while the rows go up
+  int64_t nc = 0, np = 0, nu = 0;
+  s = crius_enumerate_cells(c, &nc, &np, &nu, stream);
+  if (n_cells) *n_cells = nc;
+  if (n_cell_plans) *n_cell_plans = np;
+  if (n_units) *n_units = nu;
+  if (s != CRIUS_OK) return bail(s);
+  if (nc > out_capacity)
+    return bail(fail(CRIUS_EINVAL, "update_estimate: d_out holds fewer records than n_cells (returned)"));
+  // chunk q's checks and estimate as soon as its rows are resident; records
+  // and splits at their global Cell / unit index
+  for (int q = 0; q < n_chunks; ++q) {
+    CK(cudaStreamWaitEvent(st, c->ev_chunk[q], 0));
+    s = check_rows(c, cl, &cf, J, st, jq[q], jq[q + 1]);
+    if (s == CRIUS_OK)
+      s = launch_estimate(c, 0, 0, (int64_t)jq[q] * T, (int64_t)jq[q + 1] * T, d_out, d_splits,
+                          nullptr, nullptr, st, false, true);
+    if (s != CRIUS_OK) return bail(s);
+  }
+  s = check_result(c, J, st, 0, J);
+  if (s != CRIUS_OK) c->enumerated = false;  // the estimates read rows that failed the checks
+  return s;
 }
 
 // ---- fused exchange (SURVEY §8(e) fused-collective option) -------------------
@@ -1130,6 +1260,9 @@ void crius_destroy(crius_ctx *c) {
   if (!c) return;
   crius_exchange_close(c);
   cudaSetDevice(c->device);
+  for (cudaEvent_t e : c->ev_chunk) cudaEventDestroy(e);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   free_all(c);
   delete c;
 }

@@ -52,6 +52,8 @@ struct EstArgs {
   int64_t *xflag[kMaxRanks];
   uint32_t *x_done;        // CTA completion counter (the last CTA resets it)
   int32_t per_stage;       // b_mode 0 plan evaluation: one (Cell, k, stage) per lane
+  int32_t global_out;      // records / splits at their global Cell / unit index (else
+                           // relative to the launch's first Cell / unit)
 };
 
 // One Cell record: to the caller's chunk (local index) and, with the fused
@@ -893,7 +895,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
   int32_t *PLF = (int32_t *)(PSB + Lp_);           // NEXT-2: last forced gap [Lp]
   int32_t *PGS = PLF + Lp_;                        // NEXT-2: GPUs per stage [Stop]
   const int Lp = A.Lp;
-  const int64_t out_cell_base = A.ucb[A.unit_begin];
+  const int64_t out_cell_base = A.global_out ? 0 : A.ucb[A.unit_begin];
 
   int64_t un = 0;
   if (lane == 0) un = A.unit_begin + atomicAdd(A.work_counter, 1);
@@ -917,7 +919,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : C
     const int t = (int)(u % P.T);
     const int64_t cb = m.cb;
     const int nc = (int)(m.ce - cb);
-    int16_t *split_out = A.splits ? A.splits + (u - A.unit_begin) * A.split_stride : nullptr;
+    int16_t *split_out =
+        A.splits ? A.splits + (u - (A.global_out ? 0 : A.unit_begin)) * A.split_stride : nullptr;
     if (nc == 0) {
       if (split_out)
         for (int q = lane; q < A.split_stride; q += 32) split_out[q] = -1;

@@ -320,6 +320,57 @@ def test_update_profiles_and_repeat(crius, oracle_mod):
     assert np.array_equal(r2, t_ns)
 
 
+@pytest.mark.parametrize("cfg,chunks", [(2, 1), (2, 5), (3, 64), (4, 4)])
+def test_update_estimate_pipelined(crius, oracle_mod, cfg, chunks):
+    """crius_update_estimate (row upload pipelined against the per-range checks
+    and estimates, records at global Cell index) from pinned host arrays: same
+    records and splits as update + enumerate + estimate, and the oracle's."""
+    import torch
+    pkg = crius
+    a, b = W.make_config(cfg, seed=5), W.make_config(cfg, seed=5)
+    b.c = (b.c * 3).astype(np.int32)
+    b.tpv = b.tpv + 11
+    for k in ("c", "w", "act", "bnd", "tpv", "tpn"):
+        setattr(b, k, torch.from_numpy(np.ascontiguousarray(getattr(b, k))).pin_memory().numpy())
+    with pkg.Crius(a) as cr:
+        cr.enumerate()
+        cr.estimate()
+        u = cr.n_units
+        sp = torch.full((u * cr.split_stride(),), -7, dtype=torch.int16, device="cuda")
+        got = cr.update_estimate(b, chunks=chunks, splits=sp)
+        t_got, plan_got, _ = pkg.decode(got)
+        n = cr.n_cells
+        sp2 = torch.full_like(sp, -7)
+        cr.update(b)
+        cr.enumerate()
+        ref = cr.estimate(splits=sp2)
+        t_ref, plan_ref, _ = pkg.decode(ref)
+    assert np.array_equal(t_got[:n], t_ref[:n]) and np.array_equal(plan_got[:n], plan_ref[:n])
+    assert torch.equal(sp, sp2)
+    _, _, o_t, o_plan, _ = oracle_run(oracle_mod, b)
+    assert np.array_equal(t_got[:n], o_t) and np.array_equal(plan_got[:n], o_plan)
+
+
+def test_update_estimate_rejects_bad_rows(crius, oracle_mod):
+    """A row failing the bound checks: EINVAL naming the job, the records are
+    not usable (estimate before a new enumeration is refused), and a valid batch
+    afterwards works again."""
+    pkg = crius
+    a, b = W.make_config(2), W.make_config(2)
+    b.c = b.c.copy()
+    b.c.reshape(-1)[int(b.layer_off[7]) + 1] = 0
+    with pkg.Crius(a) as cr:
+        cr.enumerate()
+        with pytest.raises(pkg.CriusError) as e:
+            cr.update_estimate(b, chunks=3)
+        assert e.value.code == 2
+        with pytest.raises(pkg.CriusError):
+            cr.estimate()
+        got = pkg.decode(cr.update_estimate(a, chunks=3))[0][:cr.n_cells]
+    _, _, o_t, _, _ = oracle_run(oracle_mod, a)
+    assert np.array_equal(got, o_t)
+
+
 def test_update_profiles_range(crius, oracle_mod):
     """crius_update_profiles_range: only the rows of jobs [j0, j1) are re-copied,
     so the library estimates only units of those jobs (a range reaching other
