@@ -104,8 +104,10 @@ def lib():
         L.crius_split_stride.restype = i32
         L.crius_partition_units.argtypes = [vp, i32, vp, vp, vp]
         L.crius_estimate_cells.argtypes = [vp, i64, i64, vp, vp, vp]
-        L.crius_update_estimate.argtypes = [vp, C.POINTER(_Cluster), C.POINTER(_Jobs), i32, vp, i64,
-                                            vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), vp]
+        if hasattr(L, "crius_update_estimate"):  # (absent from older builds used in A/B runs)
+            L.crius_update_estimate.argtypes = [vp, C.POINTER(_Cluster), C.POINTER(_Jobs), i32, vp,
+                                                i64, vp, C.POINTER(i64), C.POINTER(i64),
+                                                C.POINTER(i64), vp]
         L.crius_estimate_assembled.argtypes = [vp, C.POINTER(_Assembly), i64, i64, vp, vp, vp]
         L.crius_tune_assembled.argtypes = [vp, i32, i64, i64, vp, vp, vp, vp]
         L.crius_estimate_paper_stages.argtypes = [vp, i64, i64, vp, vp, vp, vp]

@@ -865,8 +865,15 @@ __device__ __forceinline__ UnitMeta load_meta(const Params &P, const EstArgs &A,
 #ifndef CRIUS_EST_MINB_WIDE
 #define CRIUS_EST_MINB_WIDE 3
 #endif
+// NEXT-1..3 (AMODE > 0) keep <= 128 registers: at 80 the assembly kernel spills
+// (cfg4 NEXT-1 estimate 3.05 -> 3.47 ms)
+#ifndef CRIUS_EST_MINB_ASM
+#define CRIUS_EST_MINB_ASM 4
+#endif
 template <int WARPS, int NBG, int AMODE>
-__global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE : CRIUS_EST_MINB) * 4 / WARPS)
+__global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE
+                                                       : (AMODE == 0 ? CRIUS_EST_MINB : CRIUS_EST_MINB_ASM)) *
+                                                  4 / WARPS)
     k_estimate(Params P, EstArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
