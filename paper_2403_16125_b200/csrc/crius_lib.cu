@@ -1170,7 +1170,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   R.glob = c->adm_glob;
   R.ord = c->d_ord;
   R.osc = c->d_osc;
-  k_round_options<<<(J + 127) / 128, 128, 0, st>>>(c->P, c->C.unit_cell_begin, c->C.type, c->C.G,
+  k_round_options_warp<<<(unsigned)(((int64_t)J * 32 + 127) / 128), 128, 0, st>>>(c->P, c->C.unit_cell_begin, c->C.type, c->C.G,
                                                    (const CellResult *)d_all, R);
   CKL();
   // K6 keeps the admitted records in dynamic shared memory when its own bound

@@ -8,7 +8,7 @@
 //             G <= N_G, else ScaleResource with <= d victim moves
 //   Phase B = extra scheduling / reverse scaling, d sweeps
 //
-// K5 builds O_j for every job in priority order (one thread per job), plus the
+// K5 builds O_j for every job in priority order (one warp per job), plus the
 // job's arrival options (G <= N_G) in kappa order, transposed [k][J] so that
 // one thread per job reads them coalesced.
 //
@@ -118,128 +118,155 @@ __device__ __forceinline__ bool kappa_less(const OptRec &a, const OptRec &b) {
   return a.t < b.t;
 }
 
-// K5: per job (thread), options, ref and scores from its Cells (contiguous,
-// (t, G, S) order), written at the job's priority position; the arrival
-// options in kappa order; per-type smallest G and first index.  The options
-// are built in a thread-local buffer (OB: kLocalOpt entries, L1-resident) when
-// they fit, else in place in the global table.
-constexpr int kLocalOpt = 32;
-template <bool kLocal>
-__device__ __forceinline__ void round_options_job(const Params &P, const int64_t *__restrict__ ucb,
-                                                  const int32_t *__restrict__ cType,
-                                                  const int32_t *__restrict__ cG,
-                                                  const CellResult *__restrict__ res, const RoundBuf &R,
-                                                  int j) {
+// K5, one warp per job: its options O_j (per (t, G) the Cell with min (T, S),
+// A-17), ref and scores from its Cells (contiguous, (t, G, S) order), written
+// at the job's priority position; the arrival options (G <= N_G) in kappa
+// order, transposed; per-type smallest G and first index; the options in
+// score order.  Lanes take the Cells 32 at a time: an option is a run of equal
+// (t, G) among the accepted Cells and keeps its smallest T (the earliest Cell,
+// i.e. the smallest S, on ties); the rankings are counts over the job's
+// options, one option per lane.
+__device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
+#pragma unroll
+  for (int d = 16; d; d >>= 1) v = min(v, (int64_t)__shfl_xor_sync(0xffffffffu, v, d));
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_or_u64(uint64_t v) {
+  const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
+  const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
+  return ((uint64_t)hi << 32) | lo;
+}
+
+__global__ void k_round_options_warp(Params P, const int64_t *__restrict__ ucb,
+                                     const int32_t *__restrict__ cType, const int32_t *__restrict__ cG,
+                                     const CellResult *__restrict__ res, RoundBuf R) {
+  const int lane = threadIdx.x & 31;
+  const int j = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (j >= R.J) return;  // warp-uniform
   const int pos = R.rank[j];
   const int64_t c0 = ucb[(int64_t)j * R.T], c1 = ucb[(int64_t)(j + 1) * R.T];
   const int ngj = P.ng[j];
   OptRec *og = R.opt + (int64_t)pos * R.maxopt;
   int64_t *ocg = R.opt_cell + (int64_t)pos * R.maxopt;
-  OptRec ol[kLocal ? kLocalOpt : 1];
-  int64_t ocl[kLocal ? kLocalOpt : 1];
-  OptRec *o = kLocal ? ol : og;
-  int64_t *oc = kLocal ? ocl : ocg;
-  int n = 0;
-  int64_t ref_ng = kInf, ref_any = kInf;
-  int lastT = -1, lastG = -1;
+  double *sc = R.score + (int64_t)pos * R.maxopt;
   const bool act = R.active ? R.active[j] != 0 : true;
   const int64_t rc0 = (act && R.run_cell) ? R.run_cell[j] : -1;
   const int rct = rc0 >= 0 ? cType[rc0] : -1, rcG = rc0 >= 0 ? cG[rc0] : -1;
   const int64_t tmx = R.tmax ? R.tmax[j] : kInf;
-#pragma unroll 4
-  for (int64_t c = c0; c < c1; ++c) {
+  const uint32_t lt = (1u << lane) - 1;
+  // ref (A-16): best T at G = N_G, else best overall, over the feasible Cells
+  int64_t rng = kInf, rany = kInf;
+  for (int64_t c = c0 + lane; c < c1; c += 32) {
     const int64_t T = res[c].t_ns;
-    const int t = cType[c], G = cG[c];
     if (T == kInf) continue;
-    ref_any = min(ref_any, T);
-    if (G == ngj) ref_ng = min(ref_ng, T);
-    if ((R.policy & 1) && G != ngj) continue;  // NA: the job stays at N_G GPUs
-    // deadline: a Cell slower than the job's bound is no option, except the
-    // (type, G) the job runs on (its completion was guaranteed at placement)
-    if (T > tmx && !(t == rct && G == rcG)) continue;
-    if (t == lastT && G == lastG) {
-      if (T < o[n - 1].T) {  // equal T keeps the earlier (smaller S) Cell
-        o[n - 1].T = T;
-        oc[n - 1] = c;
+    rany = min(rany, T);
+    if (cG[c] == ngj) rng = min(rng, T);
+  }
+  rng = warp_min_i64(rng);
+  rany = warp_min_i64(rany);
+  const int64_t ref = rng != kInf ? rng : rany;
+  // options: runs of equal (t, G) among the accepted Cells
+  int n = 0, kt = -1, kG = -1;  // options so far; (t, G) of the last accepted Cell
+  int64_t kT = kInf;            // the best T of the last option so far
+  for (int64_t b0 = c0; b0 < c1; b0 += 32) {
+    const int64_t c = b0 + lane;
+    int64_t T = kInf;
+    int t = -1, G = -1;
+    if (c < c1) {
+      T = res[c].t_ns;
+      t = cType[c];
+      G = cG[c];
+    }
+    bool acc = T != kInf;
+    if ((R.policy & 1) && G != ngj) acc = false;  // NA: the job stays at N_G GPUs
+    if (T > tmx && !(t == rct && G == rcG)) acc = false;  // deadline (R-12)
+    const uint32_t am = __ballot_sync(0xffffffffu, acc);
+    const uint32_t below = am & lt;
+    const int pl = below ? 31 - __clz(below) : -1;  // previous accepted lane
+    const int pt = __shfl_sync(0xffffffffu, t, max(pl, 0)), pG = __shfl_sync(0xffffffffu, G, max(pl, 0));
+    const bool head = acc && (pl >= 0 ? (t != pt || G != pG) : (t != kt || G != kG));
+    const uint32_t hm = __ballot_sync(0xffffffffu, head);
+    const int oi = n - 1 + __popc(hm & (lt | (1u << lane)));  // this lane's option
+    // per option of the chunk: smallest T, lowest lane (= earliest Cell) on ties
+    const uint32_t gm = __match_any_sync(0xffffffffu, acc ? oi : -1 - lane);
+    const uint32_t hi = (uint32_t)((uint64_t)T >> 32), lo = (uint32_t)T;
+    const uint32_t mhi = __reduce_min_sync(gm, hi);
+    const uint32_t mlo = __reduce_min_sync(gm, hi == mhi ? lo : 0xffffffffu);
+    const int64_t gmin = (int64_t)(((uint64_t)mhi << 32) | mlo);
+    const uint32_t wm = __ballot_sync(0xffffffffu, acc && T == gmin) & gm;
+    if (acc && lane == __ffs(wm) - 1) {
+      if (oi >= n) {  // a run that starts in this chunk
+        og[oi].T = T;
+        og[oi].G = G;
+        og[oi].t = t;
+        ocg[oi] = c;
+      } else if (T < kT) {  // the run carried over: strictly better replaces
+        og[oi].T = T;
+        ocg[oi] = c;
       }
-    } else {
-      o[n].T = T;
-      o[n].G = G;
-      o[n].t = t;
-      oc[n] = c;
-      ++n;
-      lastT = t;
-      lastG = G;
+    }
+    if (am) {
+      const int ll = 31 - __clz(am);  // last accepted lane
+      const int loi = __shfl_sync(0xffffffffu, oi, ll);
+      const int64_t lmin = __shfl_sync(0xffffffffu, gmin, ll);
+      kT = loi == n - 1 ? min(kT, lmin) : lmin;
+      kt = __shfl_sync(0xffffffffu, t, ll);
+      kG = __shfl_sync(0xffffffffu, G, ll);
+      n += __popc(hm);
     }
   }
-  const int64_t ref = ref_ng != kInf ? ref_ng : ref_any;
-  double *sc = R.score + (int64_t)pos * R.maxopt;
-  double sl[kLocal ? kLocalOpt : 1];
-  double *scw = kLocal ? sl : sc;
-  uint64_t gmb = ~0ull, tsv = ~0ull;
-  for (int i = 0; i < n; ++i) {
-    const OptRec x = o[i];
-    if (kLocal) {
-      og[i] = x;
-      ocg[i] = oc[i];
-    }
-    const double si = score_of(ref, x.T);
-    sc[i] = si;
-    if (kLocal) sl[i] = si;
-    const int sh = 8 * x.t;
-    if (((gmb >> sh) & 0xff) == 0xff) {  // first (smallest G) option of its type
-      gmb = (gmb & ~(0xffull << sh)) | ((uint64_t)ilog2_pow2((uint32_t)x.G) << sh);
-      tsv = (tsv & ~(0xffull << sh)) | ((uint64_t)i << sh);
-    }
-  }
-  R.gminb[pos] = gmb;
-  R.tsb[pos] = tsv;
-  // options by score descending (the order of loss = score(cur) - score(o'))
-  uint8_t *pm = R.operm + (int64_t)pos * R.maxopt;
-  for (int i = 0; i < n; ++i) {
-    const double si = scw[i];
-    int r = 0;
-    for (int i2 = 0; i2 < n; ++i2) r += scw[i2] > si || (scw[i2] == si && i2 < i);
-    pm[r] = (uint8_t)i;
-  }
-  // arrival options (G <= N_G) in kappa order: rank by counting
-  int na = 0;
-  for (int i = 0; i < n; ++i) {
-    const OptRec x = o[i];
-    if (x.G > ngj) continue;
-    int r = 0;
-    for (int i2 = 0; i2 < n; ++i2) {
-      const OptRec y = o[i2];
-      r += (y.G <= ngj && kappa_less(y, x));
-    }
-    R.ao_pk[(int64_t)r * R.J + pos] = i | (ilog2_pow2((uint32_t)x.G) << 8) | (x.t << 13);
-    R.ao_sc[(int64_t)r * R.J + pos] = score_of(ref, x.T);
-    ++na;
-  }
-  R.nao[pos] = na;
-  R.nopt[pos] = n;
-  R.ref[pos] = ref;
-  R.cur[pos] = -1;
-  // round state: a running job keeps the option of its Cell's (type, G)
+  __syncwarp();
+  // scores, per-type first option, running option
+  uint64_t gv = 0, tv = 0, pres = 0;
   int ro = -1;
-  if (rc0 >= 0) {
-    for (int i = 0; i < n; ++i)
-      if (o[i].t == rct && o[i].G == rcG) ro = i;
-    if (ro < 0) atomicExch(R.err, 1);  // the oracle rejects this input (status 2)
+  for (int i = lane; i < n; i += 32) {
+    const OptRec x = og[i];
+    sc[i] = score_of(ref, x.T);
+    if (i == 0 || og[i - 1].t != x.t) {  // first (smallest G) option of its type
+      const int sh = 8 * x.t;
+      gv |= (uint64_t)ilog2_pow2((uint32_t)x.G) << sh;
+      tv |= (uint64_t)i << sh;
+      pres |= 0xffull << sh;
+    }
+    if (x.t == rct && x.G == rcG) ro = i;
   }
-  R.run_opt[pos] = ro;
-  R.cand[pos] = (int8_t)(act && ro < 0 && ref != kInf && na > 0);
-}
-
-__global__ void k_round_options(Params P, const int64_t *__restrict__ ucb,
-                                const int32_t *__restrict__ cType, const int32_t *__restrict__ cG,
-                                const CellResult *__restrict__ res, RoundBuf R) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= R.J) return;
-  if (R.maxopt <= kLocalOpt)
-    round_options_job<true>(P, ucb, cType, cG, res, R, j);
-  else
-    round_options_job<false>(P, ucb, cType, cG, res, R, j);
+  gv = warp_or_u64(gv);
+  tv = warp_or_u64(tv);
+  pres = warp_or_u64(pres);
+  ro = __reduce_max_sync(0xffffffffu, (unsigned)(ro + 1)) - 1;
+  __syncwarp();
+  // arrival options (G <= N_G) in kappa order; all options in score order
+  uint8_t *pm = R.operm + (int64_t)pos * R.maxopt;
+  int na = 0;
+  for (int i = lane; i < n; i += 32) {
+    const OptRec x = og[i];
+    const double si = sc[i];
+    int rk = 0, rs = 0;
+    for (int i2 = 0; i2 < n; ++i2) {
+      const OptRec y = og[i2];
+      const double s2 = sc[i2];
+      rk += (y.G <= ngj && kappa_less(y, x));
+      rs += s2 > si || (s2 == si && i2 < i);
+    }
+    pm[rs] = (uint8_t)i;
+    if (x.G <= ngj) {
+      R.ao_pk[(int64_t)rk * R.J + pos] = i | (ilog2_pow2((uint32_t)x.G) << 8) | (x.t << 13);
+      R.ao_sc[(int64_t)rk * R.J + pos] = si;
+      ++na;
+    }
+  }
+  na = (int)__reduce_add_sync(0xffffffffu, (unsigned)na);
+  if (lane == 0) {
+    R.gminb[pos] = gv | ~pres;
+    R.tsb[pos] = tv | ~pres;
+    R.nao[pos] = na;
+    R.nopt[pos] = n;
+    R.ref[pos] = ref;
+    R.cur[pos] = -1;
+    if (rc0 >= 0 && ro < 0) atomicExch(R.err, 1);  // the oracle rejects this input (status 2)
+    R.run_opt[pos] = rc0 >= 0 ? ro : -1;
+    R.cand[pos] = (int8_t)(act && ro < 0 && ref != kInf && na > 0);
+  }
 }
 
 // ---- warp argmin by lexicographic 3-word keys, one redux.sync per word ------
