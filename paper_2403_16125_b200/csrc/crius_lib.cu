@@ -111,6 +111,7 @@ struct crius_ctx {
   double *d_ao_sc = nullptr, *d_osc = nullptr;
   uint64_t *d_gminb = nullptr, *d_tsb = nullptr;
   uint8_t *d_operm = nullptr;
+  int32_t *d_opk = nullptr;
   // crius_update_estimate: the row upload runs on its own stream, one event per chunk
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_start = nullptr;
@@ -147,7 +148,7 @@ void free_all(crius_ctx *c) {
                   c->d_counter, c->d_opt, c->d_opt_cell, c->d_ref, c->d_decision, c->d_nopt,
                   c->d_rng, c->d_cur, c->d_free, c->d_total, c->d_round_stats, c->d_score,
                   c->d_ao_pk, c->d_nao, c->d_rerr, c->d_ord, c->d_ao_sc, c->d_osc, c->d_gminb, c->d_tsb,
-                  c->d_operm, c->adm_glob.bk, c->adm_glob.bl, c->adm_glob.ek, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
+                  c->d_operm, c->d_opk, c->adm_glob.bk, c->adm_glob.bl, c->adm_glob.ek, c->adm_glob.pos, c->adm_glob.cur, c->adm_glob.G,
                   c->adm_glob.t, c->adm_glob.slot, c->adm_glob.bi, c->adm_glob.ei, c->adm_glob.tl,
                   c->adm_glob.gmb, c->adm_glob.tsb, c->adm_glob.nopt, c->adm_glob.po,
                   c->d_run_opt, c->d_cand, c->d_run_cell, c->d_active};
@@ -1087,6 +1088,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
     CK(dalloc(&c->d_ao_pk, JO));
     CK(dalloc(&c->d_ao_sc, JO));
     CK(dalloc(&c->d_operm, JO));
+    CK(dalloc(&c->d_opk, JO));
     CK(dalloc(&c->d_ref, J));
     CK(dalloc(&c->d_decision, J));
     CK(dalloc(&c->d_nopt, J));
@@ -1162,6 +1164,7 @@ crius_status crius_schedule_round_state(crius_ctx *c, const crius_cell_result *d
   R.gminb = c->d_gminb;
   R.tsb = c->d_tsb;
   R.operm = c->d_operm;
+  R.opk = c->d_opk;
   R.run_cell = run_cell ? c->d_run_cell : nullptr;
   R.active = active ? c->d_active : nullptr;
   R.run_opt = c->d_run_opt;

@@ -96,6 +96,8 @@ struct RoundBuf {
   uint64_t *tsb;         // [J] byte u = index of the job's first option on type u
   uint8_t *operm;        // [J][maxopt] by position: option indices by score descending
                          // (equal scores: lower index first)
+  int32_t *opk;          // [J][maxopt] by position: option i's pool word (log2 G | t << 8 |
+                         // operm[i] << 16), so staging an option is a plain copy
   // NEXT-4 round state (NULL = every job active, none running)
   const int64_t *run_cell;  // [J] by job: Cell the job runs on, or -1
   const uint8_t *active;    // [J] by job: the job takes part in this round
@@ -256,6 +258,12 @@ __global__ void k_round_options_warp(Params P, const int64_t *__restrict__ ucb,
     }
   }
   na = (int)__reduce_add_sync(0xffffffffu, (unsigned)na);
+  __syncwarp();
+  int32_t *pk = R.opk + (int64_t)pos * R.maxopt;
+  for (int i = lane; i < n; i += 32) {
+    const OptRec x = og[i];
+    pk[i] = ilog2_pow2((uint32_t)x.G) | (x.t << 8) | ((int)pm[i] << 16);
+  }
   if (lane == 0) {
     R.gminb[pos] = gv | ~pres;
     R.tsb[pos] = tv | ~pres;
@@ -1031,30 +1039,29 @@ constexpr int kRecBytes = 5 * 8 + 9 * 4;
 constexpr int kAO = 8;  // arrival options a batch thread keeps in registers
 
 // Warp: copy the options of records [a0, a1) into the pool (two records per
-// pass, 16 lanes each).
+// pass, 16 lanes each) with cp.async; the copying threads wait before the
+// barrier that ends the next direct evaluation (the pool is read only after it).
 __device__ __forceinline__ void stage_options(const RoundBuf &R, const AdmView &A, int a0, int a1) {
   const int lane = threadIdx.x & 31;
   for (int a = a0 + (lane >> 4); a < a1; a += 2) {
     const int po = A.po[a];
     if (po < 0) continue;
-    const int p = A.pos[a], nv = A.nopt[a];
+    const int64_t q = (int64_t)A.pos[a] * R.maxopt;
+    const int nv = A.nopt[a];
     for (int i = lane & 15; i < nv; i += 16) {
-      const OptRec o = ldg_opt(R.opt + (int64_t)p * R.maxopt + i);
-      A.ppk[po + i] = ilog2_pow2((uint32_t)o.G) | (o.t << 8) |
-                      ((int)__ldg(R.operm + (int64_t)p * R.maxopt + i) << 16);
-      A.psc[po + i] = __ldg(R.score + (int64_t)p * R.maxopt + i);
+      cp_async4(A.ppk + po + i, R.opk + q + i);
+      cp_async8(A.psc + po + i, R.score + q + i);
     }
   }
 }
 
-// Warp: copy job `pos`'s nv options into the pool at po.
+// Warp: copy job `pos`'s nv options into the pool at po (cp.async, as above).
 __device__ __forceinline__ void stage_job(const RoundBuf &R, const AdmView &A, int pos, int nv, int po) {
   const int lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)pos * R.maxopt;
   for (int i = lane; i < nv; i += 32) {
-    const OptRec o = ldg_opt(R.opt + (int64_t)pos * R.maxopt + i);
-    A.ppk[po + i] = ilog2_pow2((uint32_t)o.G) | (o.t << 8) |
-                    ((int)__ldg(R.operm + (int64_t)pos * R.maxopt + i) << 16);
-    A.psc[po + i] = __ldg(R.score + (int64_t)pos * R.maxopt + i);
+    cp_async4(A.ppk + po + i, R.opk + q + i);
+    cp_async8(A.psc + po + i, R.score + q + i);
   }
 }
 
@@ -1238,6 +1245,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
     }
     __syncthreads();
     for (int a0 = 2 * wid; a0 < base; a0 += 2 * kRoundWarps) stage_options(R, A, a0, min(a0 + 2, base));
+    cp_async_wait_all();
     __syncthreads();
   }
   const int n_run = sh.n_adm;
@@ -1297,6 +1305,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
           sh.wk2[wid] = 0;
         }
       }
+      cp_async_wait_all();  // the last commit's option staging (read from here on)
       __syncthreads();
       ++n_bar;
       ++n_batches;
@@ -1526,6 +1535,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_round(RoundBuf R) {
       }
     }
   }
+  cp_async_wait_all();
+  __syncthreads();
   const long long c_phaseB = clock64();
 
   // ---- Phase B: up to d sweeps of reverse scaling over admitted jobs, in
