@@ -1200,11 +1200,37 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE
       // (integer, so the reduction order is immaterial), the group's first
       // lane holds the plan, and the segmented min-scan below picks the Cell's
       // best plan as in the per-plan path.
-      for (int i = lane; i < nc; i += 32) {
-        const int si = CS[i];
-        int r = 0;
-        for (int q = 0; q < nc; ++q) r += CS[q] > si || (CS[q] == si && q < i);
-        ORD[r] = i;
+      // counting sort by log2 S (0..5): rank = Cells with a larger S + Cells
+      // of the same S before it
+      const uint32_t lt = (1u << lane) - 1;
+      {
+        int cnt[6] = {0, 0, 0, 0, 0, 0};
+        for (int b0 = 0; b0 < nc; b0 += 32) {
+          const int i = b0 + lane;
+          const int ls = i < nc ? ilog2_pow2(CS[i]) : -1;
+#pragma unroll
+          for (int b = 0; b < 6; ++b) cnt[b] += __popc(__ballot_sync(0xffffffffu, ls == b));
+        }
+        int above[6], seen[6];
+        int acc = 0;
+#pragma unroll
+        for (int b = 5; b >= 0; --b) {
+          above[b] = acc;
+          acc += cnt[b];
+          seen[b] = 0;
+        }
+        for (int b0 = 0; b0 < nc; b0 += 32) {
+          const int i = b0 + lane;
+          const int ls = i < nc ? ilog2_pow2(CS[i]) : -1;
+          int rk = 0;
+#pragma unroll
+          for (int b = 0; b < 6; ++b) {
+            const uint32_t m = __ballot_sync(0xffffffffu, ls == b);
+            if (ls == b) rk = above[b] + seen[b] + __popc(m & lt);
+            seen[b] += __popc(m);
+          }
+          if (i < nc) ORD[rk] = i;
+        }
       }
       __syncwarp();
       {
@@ -1226,22 +1252,25 @@ __global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE
       const int nitems = CP[nc];
       int carry_r = -1, carry_p = 0;
       int64_t carry_T = kInf;
+      int rb = 0;  // the Cell holding the chunk's first item
       for (int f0 = 0; f0 < nitems; f0 += 32) {
         const int f = f0 + lane;
         const bool valid = f < nitems;
+        // item -> Cell: the Cells after rb that start inside the chunk (every
+        // Cell holds >= 1 item, so at most 31 of them), one per lane
+        const int rs = rb + 1 + lane;
+        const int st = rs < nc ? CP[rs] - f0 : 32;
+        const uint32_t starts = __reduce_or_sync(0xffffffffu, st > 0 && st < 32 ? 1u << st : 0u);
+        const int rl = rb + __popc(starts & ((2u << lane) - 1));
+        {
+          const int r31 = rb + __popc(starts);
+          rb = r31 + (r31 + 1 < nc && CP[r31 + 1] == f0 + 32 ? 1 : 0);
+        }
         int r = nc, p = 0, S = 1, s = 0, lB = 0;
         bool bad = true;
         int64_t Ts = 0, sy = 0;
         if (valid) {
-          int lo = 0, hi = nc - 1;  // largest r with CP[r] <= f
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (CP[mid] <= f)
-              lo = mid;
-            else
-              hi = mid - 1;
-          }
-          r = lo;
+          r = rl;
           const int ci = ORD[r], local = f - CP[r];
           CRIUS_CHECK(ci >= 0 && ci < nc && local >= 0 && local < CP[r + 1] - CP[r]);
           S = CS[ci];
