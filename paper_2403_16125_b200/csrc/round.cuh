@@ -981,21 +981,6 @@ __device__ __forceinline__ void gq_join(RoundShared &sh, int t, uint64_t gb) {
       __vminu4((uint32_t)g, (uint32_t)gb);
 }
 
-// Thread 0: (re)point admitted record a at option (idx, G, t).
-__device__ __forceinline__ void adm_point(RoundShared &sh, const AdmView &A, int a, int idx, int G,
-                                          int t) {
-  if (A.t[a] != t) {
-    list_remove(sh, A, a);
-    list_add(sh, A, a, t);
-    gq_join(sh, t, A.gmb[a]);
-  }
-  A.cur[a] = idx;
-  A.G[a] = G;
-  A.t[a] = t;
-  A.bi[a] = -2;
-  A.ei[a] = -1;
-  sh.vic[sh.n_vic++] = a;
-}
 // po: the record's pool offset (allocated by the caller), -1 = none
 __device__ __forceinline__ void adm_new(RoundShared &sh, const AdmView &A, int w, int pos, int idx,
                                         int G, int t, int po) {
