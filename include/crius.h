@@ -143,7 +143,10 @@ crius_status crius_update_profiles_range(crius_ctx *ctx, const crius_cluster *cl
                                          int32_t job_end, void *stream);
 
 /* Enumerate every Cell (§N2) on the device: per-unit counts, scan,
- * fill.  Synchronises `stream` and returns the counts.  EINFEASIBLE if 0 Cells. */
+ * fill.  Synchronises `stream` once, for the counts it returns; the fill of the
+ * Cell table is then queued on `stream` (work queued after it on `stream`, or
+ * anything after a synchronisation of `stream`, sees the complete table).
+ * EINFEASIBLE if 0 Cells. */
 crius_status crius_enumerate_cells(crius_ctx *ctx, int64_t *n_cells, int64_t *n_cell_plans,
                                    int64_t *n_units, void *stream);
 

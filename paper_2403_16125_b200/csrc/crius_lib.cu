@@ -570,8 +570,7 @@ crius_status crius_enumerate_cells(crius_ctx *c, int64_t *n_cells, int64_t *n_pl
   if (c->n_cells > 0) {
     k_unit_fill<<<(unsigned)((U + 255) / 256), 256, 0, st>>>(c->P, c->C, U);
     CKL();
-    c->launches += 1;
-    CK(cudaStreamSynchronize(st));
+    c->launches += 1;  // stream-ordered: no second host round trip
   }
   if (n_cells) *n_cells = c->n_cells;
   if (n_plans) *n_plans = c->n_plans;
