@@ -855,13 +855,14 @@ __device__ __forceinline__ UnitMeta load_meta(const Params &P, const EstArgs &A,
 }
 
 #ifndef CRIUS_EST_MINB
-#define CRIUS_EST_MINB 6  // <= 80 registers: 6 CTAs (24 warps) per SM
+#define CRIUS_EST_MINB 7  // <= 72 registers: 7 CTAs (28 warps) per SM
 #endif
 // The B-sweep instantiation (NBG > 1) keeps NBG partial sums per lane and spills
 // at 128 registers; its per-warp shared memory already caps it near 3 CTAs per
 // SM at large L, so it gets <= 168 registers (measured: cfg5 4.80 -> 4.34 ms,
 // cfg3 0.129 -> 0.123 ms).  The NBG = 1 kernel: 80 registers (6 CTAs, 24 warps per SM)
-// measured cfg4 0.249 vs 0.257 ms at 128 (per-plan lanes), 0.227 ms with per-stage lanes.
+// measured cfg4 0.249 vs 0.257 ms at 128 (per-plan lanes), 0.227 ms with per-stage lanes;
+// 72 registers (7 CTAs) 0.220 ms, 64 (8 CTAs) 0.227 ms (spills).
 #ifndef CRIUS_EST_MINB_WIDE
 #define CRIUS_EST_MINB_WIDE 3
 #endif
