@@ -866,15 +866,22 @@ __device__ __forceinline__ UnitMeta load_meta(const Params &P, const EstArgs &A,
 #ifndef CRIUS_EST_MINB_WIDE
 #define CRIUS_EST_MINB_WIDE 3
 #endif
-// NEXT-1..3 (AMODE > 0) keep <= 128 registers: at 80 the assembly kernel spills
-// (cfg4 NEXT-1 estimate 3.05 -> 3.47 ms)
+// NEXT-1 / NEXT-3 (AMODE 1..3) keep <= 128 registers: at 80 the assembly kernel
+// spills (cfg4 NEXT-1 estimate 3.05 -> 3.47 ms); NEXT-2 (AMODE 4) runs at 80
+// (cfg4 1.44 -> 1.38 ms)
 #ifndef CRIUS_EST_MINB_ASM
 #define CRIUS_EST_MINB_ASM 4
 #endif
+#ifndef CRIUS_EST_MINB_PAPER
+#define CRIUS_EST_MINB_PAPER 6
+#endif
 template <int WARPS, int NBG, int AMODE>
-__global__ void __launch_bounds__(WARPS * 32, (NBG > 1 ? CRIUS_EST_MINB_WIDE
-                                                       : (AMODE == 0 ? CRIUS_EST_MINB : CRIUS_EST_MINB_ASM)) *
-                                                  4 / WARPS)
+__global__ void __launch_bounds__(WARPS * 32,
+                                  (NBG > 1 ? CRIUS_EST_MINB_WIDE
+                                           : (AMODE == 0 ? CRIUS_EST_MINB
+                                                         : (AMODE == 4 ? CRIUS_EST_MINB_PAPER
+                                                                       : CRIUS_EST_MINB_ASM))) *
+                                      4 / WARPS)
     k_estimate(Params P, EstArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
